@@ -1,0 +1,138 @@
+"""CPU oracle for SCS-1 (the SAGE checksum loop, arXiv 2209.03125).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py
+(its cpu_baseline leg and --impl reference arm) may import this package.  The
+product package paper_2209_03125_b200 never imports it, and the two share no
+code: the C oracle (sage_oracle.c) and the pure-Python oracle (ref.py) are
+written from the SCS-1 text in DESIGN.md section 3.
+
+Parity status: every SCS-1 step is pinned by tests/test_oracle_pins.py (see
+DESIGN.md section 4 for the pin per step); none is "parity unpinned".
+"""
+import ctypes
+import os
+import subprocess
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sage_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force=False):
+    """Compile sage_oracle.c with gcc -O2 (plain scalar, no -march)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".%d.tmp" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        u64, u32, p = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p
+        L.sage_oracle_splitmix_mix.restype = u64
+        L.sage_oracle_splitmix_mix.argtypes = [u64]
+        L.sage_oracle_xs.restype = u64
+        L.sage_oracle_xs.argtypes = [u64]
+        L.sage_oracle_thread_init.restype = None
+        L.sage_oracle_thread_init.argtypes = [u64, u64, p, p]
+        L.sage_oracle_fold.restype = u64
+        L.sage_oracle_fold.argtypes = [p, u64]
+        L.sage_oracle_warp_rounds.restype = ctypes.c_int
+        L.sage_oracle_warp_rounds.argtypes = [p, p, p, u64, u64, u64, u64, ctypes.c_uint]
+        L.sage_oracle_warp.restype = ctypes.c_int
+        L.sage_oracle_warp.argtypes = [u64, p, u64, u64, u64, u64, ctypes.c_uint, p]
+        L.sage_oracle_attest.restype = ctypes.c_int
+        L.sage_oracle_attest.argtypes = [u64, p, u64, u64, u64, u64, u64, ctypes.c_uint, p]
+        _lib = L
+    return _lib
+
+
+def _buf(region):
+    arr = np.ascontiguousarray(np.frombuffer(bytes(region), dtype=np.uint8) if not isinstance(region, np.ndarray)
+                               else region.view(np.uint8).reshape(-1))
+    return arr, arr.ctypes.data_as(ctypes.c_void_p), arr.nbytes
+
+
+def splitmix_mix(z):
+    return lib().sage_oracle_splitmix_mix(z & (2**64 - 1))
+
+
+def xs(x):
+    return lib().sage_oracle_xs(x & (2**64 - 1))
+
+
+def thread_init(nonce, g):
+    a = np.zeros(16, dtype=np.uint32)
+    x = ctypes.c_uint64(0)
+    lib().sage_oracle_thread_init(nonce, g, a.ctypes.data_as(ctypes.c_void_p), ctypes.byref(x))
+    return [int(v) for v in a], x.value
+
+
+def fold(a, x):
+    arr = np.asarray(a, dtype=np.uint32)
+    return lib().sage_oracle_fold(arr.ctypes.data_as(ctypes.c_void_p), x)
+
+
+def warp_rounds(A, X, region, base, r_begin, r_end, P=1):
+    """Run rounds [r_begin, r_end) on an explicit warp state. A: (32,16) u32, X: (32,) u64.
+    Returns new (A, X) arrays."""
+    A = np.array(A, dtype=np.uint32).reshape(32, 16).copy()
+    X = np.array(X, dtype=np.uint64).reshape(32).copy()
+    arr, ptr, n = _buf(region)
+    rc = lib().sage_oracle_warp_rounds(A.ctypes.data_as(ctypes.c_void_p), X.ctypes.data_as(ctypes.c_void_p),
+                                       ptr, n, base, r_begin, r_end, P)
+    if rc != 0:
+        raise ValueError("oracle rejected arguments")
+    return A, X
+
+
+def warp_sum(nonce, region, base, rounds, w, P=1):
+    arr, ptr, n = _buf(region)
+    out = ctypes.c_uint64(0)
+    rc = lib().sage_oracle_warp(nonce, ptr, n, base, rounds, w, P, ctypes.byref(out))
+    if rc != 0:
+        raise ValueError("oracle rejected arguments")
+    return out.value
+
+
+def attest(nonce, region, base, rounds, blocks, threads, P=1):
+    arr, ptr, n = _buf(region)
+    out = ctypes.c_uint64(0)
+    rc = lib().sage_oracle_attest(nonce, ptr, n, base, rounds, blocks, threads, P, ctypes.byref(out))
+    if rc != 0:
+        raise ValueError("oracle rejected arguments")
+    return out.value
+
+
+# ---- multi-process driver for large configs (one warp range per task) ----------
+_pool_region = None
+
+
+def _pool_init(region_bytes):
+    global _pool_region
+    _pool_region = np.frombuffer(region_bytes, dtype=np.uint8)
+
+
+def _pool_task(args):
+    nonce, base, rounds, w0, w1, P = args
+    return [warp_sum(nonce, _pool_region, base, rounds, w, P) for w in range(w0, w1)]
+
+
+def warp_sums_parallel(nonce, region, base, rounds, warps, P=1, workers=None):
+    """Oracle warp partials for the listed warp indices, spread over host cores.
+    The per-warp function is unchanged; this only fans warps out."""
+    warps = list(warps)
+    workers = workers or len(os.sched_getaffinity(0))
+    rb = bytes(np.ascontiguousarray(region).view(np.uint8).reshape(-1)) if isinstance(region, np.ndarray) else bytes(region)
+    tasks = [(nonce, base, rounds, w, w + 1, P) for w in warps]
+    with ProcessPoolExecutor(max_workers=workers, initializer=_pool_init, initargs=(rb,)) as ex:
+        res = list(ex.map(_pool_task, tasks, chunksize=max(1, len(tasks) // (4 * workers))))
+    return {w: r[0] for w, r in zip(warps, res)}
