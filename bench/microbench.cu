@@ -1,0 +1,179 @@
+// microbench.cu -- L0 probes for the integer-pipe roofline.
+//
+// Each probe runs at full occupancy (2 CTAs x 1024 threads per SM, <= 32 regs)
+// a loop of independent dependency chains of one SASS op class, and reports
+// warp-instructions issued per SM per cycle (clock64 around the loop, max over
+// CTAs) -- i.e. the measured issue rate of that op class on sm_100a.  Also a
+// random SMEM gather and a dependent random HBM gather at full occupancy.
+// Output: one JSON line per probe.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                  \
+    do {                                                                       \
+        cudaError_t e = (x);                                                   \
+        if (e != cudaSuccess) {                                                \
+            fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e));            \
+            exit(1);                                                           \
+        }                                                                      \
+    } while (0)
+
+struct Args {
+    uint32_t iters;
+    uint32_t c0, c1, c2, c3;   // runtime constants (defeat strength reduction)
+    unsigned long long* cycles;
+    uint32_t* sink;
+};
+
+constexpr int CH = 8;   // independent chains per thread
+
+#define PROBE(NAME, BODY)                                                          \
+    __global__ void __launch_bounds__(1024, 2) NAME(Args a) {                      \
+        uint32_t v[CH];                                                            \
+        _Pragma("unroll") for (int k = 0; k < CH; ++k) v[k] = threadIdx.x * (k + 3) + a.c3; \
+        __syncthreads();                                                           \
+        long long t0 = clock64();                                                  \
+        _Pragma("unroll 1") for (uint32_t it = 0; it < a.iters; ++it) {             \
+            _Pragma("unroll") for (int u = 0; u < 4; ++u) {                        \
+                _Pragma("unroll") for (int k = 0; k < CH; ++k) { BODY; }           \
+            }                                                                      \
+        }                                                                          \
+        __syncthreads();                                                           \
+        long long t1 = clock64();                                                  \
+        uint32_t s = 0;                                                            \
+        _Pragma("unroll") for (int k = 0; k < CH; ++k) s ^= v[k];                  \
+        if (s == 0x12345679u) a.sink[0] = s;                                       \
+        if (threadIdx.x == 0) atomicMax(a.cycles, (unsigned long long)(t1 - t0));  \
+    }
+
+// IMAD with a constant-bank multiplier: v = v * c0 + c1      (FMA pipe)
+PROBE(p_imad, v[k] = v[k] * v[(k + 1) & (CH - 1)] + a.c1)
+// LOP3: v = v ^ (v >> 0)... use a 3-input logic op on registers (ALU pipe)
+PROBE(p_lop3, asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[k]) : "r"(a.c0), "r"(a.c1)))
+// IADD3
+PROBE(p_iadd3, v[k] = v[k] + v[(k + 1) & (CH - 1)] + a.c1)
+// SHF (funnel shift by immediate)
+PROBE(p_shf, v[k] = __funnelshift_l(v[k], v[k], 7))
+// LEA.HI-form: v = c + rotl(v, 7)
+PROBE(p_leahi, v[k] = a.c0 + __funnelshift_l(v[k], v[k], 7))
+// IMAD.WIDE.U32: 64-bit product, keep both halves
+// multiply-with-carry on a 64-bit chain pair: one IMAD.WIDE.U32 lo, c, {hi} per body
+PROBE(p_imadwide, { if (k < CH / 2) { unsigned long long w = ((unsigned long long)v[2 * k + 1] << 32) | v[2 * k];
+                    w = (unsigned long long)v[2 * k] * a.c0 + (w >> 32); v[2 * k] = (uint32_t)w; v[2 * k + 1] = (uint32_t)(w >> 32); } })
+// IMAD.HI.U32
+PROBE(p_imadhi, v[k] = __umulhi(v[k], v[(k + 1) & (CH - 1)]) + a.c1)
+// 1:1 IMAD + LEA.HI (the R7 pattern)
+PROBE(p_mix11, { v[k] = v[k] * a.c0 + a.c1; v[k] = a.c2 + __funnelshift_l(v[k], v[k], 7); })
+
+__global__ void __launch_bounds__(1024, 2) p_smem_gather(Args a) {
+    __shared__ uint32_t s[8192];
+    for (int i = threadIdx.x; i < 8192; i += blockDim.x) s[i] = i * 2654435761u;
+    __syncthreads();
+    uint32_t x = threadIdx.x * 0x9E3779B9u + a.c3;
+    long long t0 = clock64();
+    for (uint32_t it = 0; it < a.iters * 4; ++it) {
+        x = x * 1664525u + 1013904223u;
+        x += s[x >> 19];
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (x == 0x12345679u) a.sink[0] = x;
+    if (threadIdx.x == 0) atomicMax(a.cycles, (unsigned long long)(t1 - t0));
+}
+
+__global__ void __launch_bounds__(1024, 2) p_hbm_gather(Args a, const uint32_t* __restrict__ buf, uint32_t mask) {
+    uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) * 0x9E3779B9u + a.c3;
+    long long t0 = clock64();
+    for (uint32_t it = 0; it < a.iters; ++it) {
+        x = x * 1664525u + 1013904223u;
+        uint32_t w;
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w) : "l"(buf + ((x >> 3) & mask) * 8u));
+        x ^= w;
+    }
+    long long t1 = clock64();
+    if (x == 0x12345679u) a.sink[0] = x;
+    if (threadIdx.x == 0) atomicMax(a.cycles, (unsigned long long)(t1 - t0));
+}
+
+int main() {
+    int dev = 0, sms = 0, clk = 0;
+    CK(cudaSetDevice(dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
+    Args a{};
+    a.c0 = 33; a.c1 = 0x9E3779B9u; a.c2 = 12345; a.c3 = 7;
+    CK(cudaMalloc(&a.cycles, 8));
+    CK(cudaMalloc(&a.sink, 4));
+    const int blocks = 2 * sms, threads = 1024, warps_per_sm = 64;
+    struct P { const char* name; void (*fn)(Args); int ops_per_body; };
+    P probes[] = {{"imad_const", p_imad, 1}, {"lop3", p_lop3, 1}, {"iadd", p_iadd3, 1}, {"shf_funnel", p_shf, 1},
+                  {"lea_hi_form", p_leahi, 1}, {"imad_wide_u32+iadd3", p_imadwide, -16}, {"imad_hi_u32", p_imadhi, 1},
+                  {"imad+lea_hi", p_mix11, 2}};
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (auto& p : probes) {
+        a.iters = 4096;
+        for (int rep = 0; rep < 2; ++rep) {
+            CK(cudaMemset(a.cycles, 0, 8));
+            CK(cudaEventRecord(e0));
+            p.fn<<<blocks, threads>>>(a);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+        }
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        unsigned long long cyc = 0;
+        CK(cudaMemcpy(&cyc, a.cycles, 8, cudaMemcpyDeviceToHost));
+        // per thread; a negative ops_per_body means that many bodies per iteration
+        double bodies = double(a.iters) * (p.ops_per_body < 0 ? -p.ops_per_body : 4 * CH);
+        double warp_bodies_per_sm_cycle = bodies * warps_per_sm / double(cyc);
+        double eff_mhz = double(cyc) / (ms * 1e3);
+        printf("{\"probe\": \"%s\", \"warp_bodies_per_sm_clk\": %.4f, \"src_ops_per_body\": %d, \"cycles\": %llu, "
+               "\"ms\": %.4f, \"eff_mhz\": %.1f}\n",
+               p.name, warp_bodies_per_sm_cycle, p.ops_per_body, cyc, ms, eff_mhz);
+    }
+    {   // random SMEM gather, 32 KiB table: LCG (IMAD) + shift + LDS + add per body
+        a.iters = 4096;
+        for (int rep = 0; rep < 2; ++rep) {
+            CK(cudaMemset(a.cycles, 0, 8));
+            CK(cudaEventRecord(e0));
+            p_smem_gather<<<blocks, threads>>>(a);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+        }
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        unsigned long long cyc = 0;
+        CK(cudaMemcpy(&cyc, a.cycles, 8, cudaMemcpyDeviceToHost));
+        double bodies = double(a.iters) * 4;
+        printf("{\"probe\": \"smem_random_gather\", \"warp_bodies_per_sm_clk\": %.4f, \"cycles\": %llu, \"ms\": %.4f}\n",
+               bodies * warps_per_sm / double(cyc), cyc, ms);
+    }
+    for (size_t gib : {1, 4}) {   // dependent random 4-B loads, one per 32-B sector, over gib GiB
+        size_t bytes = gib << 30;
+        uint32_t* buf = nullptr;
+        CK(cudaMalloc(&buf, bytes));
+        CK(cudaMemset(buf, 1, bytes));
+        uint32_t mask = uint32_t(bytes / 32 - 1);
+        a.iters = 2048;
+        for (int rep = 0; rep < 2; ++rep) {
+            CK(cudaMemset(a.cycles, 0, 8));
+            CK(cudaEventRecord(e0));
+            p_hbm_gather<<<blocks, threads>>>(a, buf, mask);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+        }
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        double picks = double(blocks) * threads * a.iters;
+        printf("{\"probe\": \"hbm_dependent_sector_gather\", \"gib\": %zu, \"picks_per_s\": %.4e, "
+               "\"sector_gbps\": %.1f, \"ms\": %.3f}\n", gib, picks / (ms * 1e-3), picks * 32 / (ms * 1e-3) / 1e9, ms);
+        CK(cudaFree(buf));
+    }
+    return 0;
+}

@@ -1,0 +1,145 @@
+/*
+ * sage.h -- C ABI of the B200-native SAGE checksum hot path (libsage.so).
+ *
+ * The operation is the self-verifying checksum function of SAGE
+ * (arXiv 2209.03125, section 5.2.2; loop steps at
+ * lines 634-657): every resident thread is seeded from the verifier's challenge
+ * (P:383-389), runs `rounds` iterations that read a pseudo-randomly chosen piece
+ * of the checksummed region and fold it, the data pointer and the round index
+ * into an ordered integer state, and the per-thread states are
+ * summed warp -> block -> grid into one value.  The exact
+ * arithmetic is SCS-1.
+ *
+ * Conventions for every function:
+ *   - returns SAGE_OK (0) or a negative SAGE_E* code; never throws/aborts;
+ *   - output structs are written only on success;
+ *   - a wrong checksum is not an error: comparing against the expected value
+ *     is the verifier's job;
+ *   - sage_last_error() returns a thread-local detail string for the last failure.
+ *
+ * Ownership: the caller owns `region` (a device pointer, or a host pointer for
+ * sage_attest_host) and must keep it alive and unmodified until the call
+ * returns (for sage_attest_async: until the stream work completes).  The
+ * result depends on the region's DEVICE virtual address because the data
+ * pointer is folded in every round.  The context owns its result
+ * buffers, its staging buffer for host regions and, when the config's stream is
+ * NULL, its stream.
+ */
+#ifndef SAGE_H
+#define SAGE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAGE_OK            0
+#define SAGE_EINVAL       -1  /* bad argument (see each function) */
+#define SAGE_EUNSUPPORTED -2  /* valid but not supported here (e.g. forced SMEM too large) */
+#define SAGE_ENOMEM       -3  /* device or pinned host allocation failed */
+#define SAGE_ECUDA        -4  /* CUDA runtime error; detail in sage_last_error() */
+
+/* region placement */
+#define SAGE_AUTO   0u  /* SMEM when the region fits at the launch's occupancy, else GLOBAL */
+#define SAGE_SMEM   1u  /* region staged once per CTA into shared memory (TMA bulk copy) */
+#define SAGE_GLOBAL 2u  /* region read in place from L2/HBM every round */
+
+typedef struct sage_ctx sage_ctx;
+
+typedef struct {
+    int      device;      /* CUDA device ordinal */
+    uint32_t blocks;      /* grid size; 0 => 2 * SM count (full occupancy) */
+    uint32_t threads;     /* block size, multiple of 32, <= 1024; 0 => 1024 */
+    uint32_t pick_words;  /* P, words read per round: 1, 4 or 8; 0 => 1 */
+    uint32_t placement;   /* SAGE_AUTO | SAGE_SMEM | SAGE_GLOBAL */
+    void*    stream;      /* cudaStream_t to launch on (borrowed); NULL => ctx-owned stream */
+} sage_config;
+
+typedef struct {
+    uint64_t checksum;    /* sum over all threads of the folded state, mod 2^64 */
+    uint64_t cycles;      /* max over CTAs of the CTA's clock64 duration */
+    uint64_t elapsed_ns;  /* host CLOCK_MONOTONIC from before launch to result on host (t1 - t0) */
+    uint64_t device_ns;   /* %globaltimer: last CTA end - first CTA start */
+    uint64_t region_va;   /* device VA the region was read from (the `base` of SCS-1) */
+    uint32_t placement;   /* SAGE_SMEM or SAGE_GLOBAL actually used */
+    uint32_t blocks;      /* grid actually launched */
+    uint32_t threads;     /* block size actually launched */
+    uint32_t pick_words;  /* P actually used */
+} sage_result;
+
+typedef struct {
+    int      device;
+    uint32_t sm_count;         /* cudaDevAttrMultiProcessorCount */
+    uint32_t blocks, threads, pick_words, placement;
+    uint32_t ctas_per_sm_smem; /* resident CTAs/SM of the SMEM kernel with a 64 KiB region */
+    uint32_t ctas_per_sm_global;
+    uint32_t regs_per_thread;  /* of the P-specific SMEM kernel */
+    uint64_t smem_region_max;  /* largest region (bytes) SAGE_AUTO stages into SMEM */
+} sage_info;
+
+/* Create a context on cfg->device.  cfg may be NULL (all defaults).
+ * SAGE_EINVAL: threads % 32 != 0 or > 1024, pick_words not in {1,4,8},
+ *              placement unknown, out NULL.  SAGE_ECUDA / SAGE_ENOMEM. */
+int sage_checksum_init(const sage_config* cfg, sage_ctx** out);
+
+/* Synchronous attestation over a DEVICE region (SCS-1 with base = region).
+ * region_bytes = 4 * P * Nc with Nc a power of two (<= 2^32); region 16-byte
+ * aligned (32-byte for P = 8); rounds < 2^32.  Returns when the result is on
+ * the host.  SAGE_EINVAL on a violated precondition or NULL pointer;
+ * SAGE_EUNSUPPORTED when SAGE_SMEM was forced and the region does not fit. */
+int sage_attest(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
+                uint64_t rounds, sage_result* out);
+
+/* As sage_attest, and also writes the per-warp partial sums (n/32 u64, device
+ * pointer, warp w = threads 32w..32w+31) so large configs can be checked on
+ * sampled warps: sum of partials == checksum (mod 2^64). */
+int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
+                      uint64_t rounds, uint64_t* per_warp_out, sage_result* out);
+
+/* Asynchronous form: validates, then enqueues the checksum kernel on the
+ * context's stream and returns.  raw_out is a DEVICE buffer of 4 u64 that the
+ * kernel accumulates into and that the caller zeroes before the launch
+ * (sage_attest_async zeroes it on the same stream unless it is NULL):
+ *   raw_out[0] checksum, [1] max CTA cycles, [2] ~(first CTA start ns),
+ *   [3] last CTA end ns.  per_warp_out may be NULL.  Decode with
+ *   sage_decode_raw.  Safe to capture in a CUDA graph. */
+int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
+                      uint64_t rounds, uint64_t* raw_out, uint64_t* per_warp_out);
+
+/* Decode a raw 4 x u64 result (host copy) into checksum / cycles / device_ns. */
+int sage_decode_raw(const uint64_t raw[4], sage_result* out);
+
+/* End-to-end form over a HOST region: copies the region host->device into a
+ * context-owned device buffer (whose VA is reported in out->region_va and is
+ * the SCS-1 base), attests, copies the 32-byte result back.  elapsed_ns covers
+ * the copies.  Pinned host memory gives the fastest copy. */
+int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, size_t region_bytes,
+                     uint64_t rounds, sage_result* out);
+
+/* Device VA of the context-owned staging buffer sage_attest_host would use
+ * for a region of region_bytes (allocating it if needed), so a verifier can
+ * precompute the expected checksum ahead of time. */
+int sage_host_region_va(sage_ctx* ctx, size_t region_bytes, uint64_t* va_out);
+
+/* Placement the context would choose for region_bytes (SAGE_SMEM/SAGE_GLOBAL). */
+int sage_placement_for(sage_ctx* ctx, size_t region_bytes, uint32_t* placement_out);
+
+int sage_query(sage_ctx* ctx, sage_info* out);
+
+/* Number of checksum-kernel launches this context has issued. */
+uint64_t sage_launch_count(const sage_ctx* ctx);
+
+/* cudaStream_t the context launches on. */
+void* sage_stream(const sage_ctx* ctx);
+
+void sage_checksum_destroy(sage_ctx* ctx);
+
+const char* sage_strerror(int code);
+const char* sage_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAGE_H */

@@ -1,0 +1,338 @@
+// sage_api.cu -- host runtime behind include/sage.h (libsage.so).
+//
+// Validation, placement choice, occupancy check, launch of the sm_100a
+// checksum kernel (sage_kernel.cuh), pinned result readback and host timing
+// (the verifier's t0/t1).
+#include <cuda_runtime.h>
+#include <time.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "sage.h"
+#include "sage_kernel.cuh"
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+int fail(int code, const char* fmt, const char* detail = "") {
+    snprintf(g_last_error, sizeof(g_last_error), fmt, detail);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+    return SAGE_ECUDA;
+}
+
+#define CUDA_TRY(expr)                                         \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);    \
+    } while (0)
+
+uint64_t now_ns() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return static_cast<uint64_t>(ts.tv_sec) * 1000000000ull + static_cast<uint64_t>(ts.tv_nsec);
+}
+
+#ifndef SAGE_UNROLL
+#define SAGE_UNROLL 1
+#endif
+constexpr int kUnroll = SAGE_UNROLL;
+constexpr size_t kSmemRegionMax = 64 * 1024;   // 2 CTAs/SM x 64 KiB fits the 228 KB SM
+
+using KernelFn = void (*)(const sage::KernelArgs);
+
+KernelFn kernel_for(uint32_t P, bool smem) {
+    switch (P) {
+        case 1: return smem ? sage::sage_checksum_kernel<1, true, kUnroll> : sage::sage_checksum_kernel<1, false, kUnroll>;
+        case 4: return smem ? sage::sage_checksum_kernel<4, true, kUnroll> : sage::sage_checksum_kernel<4, false, kUnroll>;
+        case 8: return smem ? sage::sage_checksum_kernel<8, true, kUnroll> : sage::sage_checksum_kernel<8, false, kUnroll>;
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+struct sage_ctx {
+    int device = 0;
+    uint32_t sm_count = 0;
+    uint32_t blocks = 0, threads = 0, pick_words = 1, placement = SAGE_AUTO;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t* d_raw = nullptr;      // 4 x u64 device result
+    uint64_t* h_raw = nullptr;      // 4 x u64 pinned host result
+    void* d_stage = nullptr;        // device copy of a host region (sage_attest_host)
+    size_t stage_bytes = 0;
+    uint64_t launches = 0;
+};
+
+namespace {
+
+int set_device(const sage_ctx* c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    return SAGE_OK;
+}
+
+// Check the SCS-1 preconditions on (region, bytes, rounds) for P.
+int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t rounds) {
+    if (c == nullptr) return fail(SAGE_EINVAL, "null context%s");
+    if (region == nullptr) return fail(SAGE_EINVAL, "null region%s");
+    const uint64_t P = c->pick_words;
+    if (bytes == 0 || bytes % (4 * P) != 0)
+        return fail(SAGE_EINVAL, "region_bytes must be a positive multiple of 4*P%s");
+    const uint64_t nc = bytes / (4 * P);
+    if ((nc & (nc - 1)) != 0 || nc > (1ull << 32))
+        return fail(SAGE_EINVAL, "region chunk count must be a power of two <= 2^32%s");
+    const uint64_t align = (4 * P > 16) ? 4 * P : 16;
+    if (reinterpret_cast<uintptr_t>(region) % align != 0)
+        return fail(SAGE_EINVAL, "region must be 16-byte aligned (32-byte for P=8)%s");
+    if (rounds > 0xFFFFFFFFull) return fail(SAGE_EINVAL, "rounds must be < 2^32%s");
+    return SAGE_OK;
+}
+
+uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
+    if (c->placement != SAGE_AUTO) return c->placement;
+    return bytes <= kSmemRegionMax ? SAGE_SMEM : SAGE_GLOBAL;
+}
+
+int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
+           uint64_t* per_warp, uint32_t* placement_used) {
+    const uint32_t placement = choose_placement(c, bytes);
+    if (placement == SAGE_SMEM && bytes > kSmemRegionMax)
+        return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s", "64 KiB");
+    const bool smem = placement == SAGE_SMEM;
+    KernelFn fn = kernel_for(c->pick_words, smem);
+    const size_t dyn = smem ? bytes : 0;
+    if (smem) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+    sage::KernelArgs args;
+    args.region = static_cast<const uint32_t*>(region);
+    args.nonce = nonce;
+    args.nc_mask = static_cast<uint32_t>(bytes / (4ull * c->pick_words) - 1);
+    args.rounds = static_cast<uint32_t>(rounds);
+    args.region_bytes = static_cast<uint32_t>(smem ? bytes : 0);
+    args.raw = raw;
+    args.per_warp = per_warp;
+    for (int j = 0; j < sage::kAccum; ++j) args.mul[j] = sage::mul_of(j);
+    fn<<<c->blocks, c->threads, dyn, c->stream>>>(args);
+    CUDA_TRY(cudaGetLastError());
+    c->launches++;
+    if (placement_used) *placement_used = placement;
+    return SAGE_OK;
+}
+
+void fill_result(const sage_ctx* c, const uint64_t raw[4], uint64_t t0, uint64_t t1, uint64_t va, uint32_t placement,
+                 sage_result* out) {
+    sage_decode_raw(raw, out);
+    out->elapsed_ns = t1 - t0;
+    out->region_va = va;
+    out->placement = placement;
+    out->blocks = c->blocks;
+    out->threads = c->threads;
+    out->pick_words = c->pick_words;
+}
+
+// attest synchronously over a device region already validated
+int attest_device(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds,
+                  uint64_t* per_warp, sage_result* out, const void* host_src) {
+    int rc = set_device(c);
+    if (rc) return rc;
+    const uint64_t t0 = now_ns();
+    if (host_src) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(region), host_src, bytes, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->d_raw, 0, 4 * sizeof(uint64_t), c->stream));
+    uint32_t placement = 0;
+    rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->h_raw, c->d_raw, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const uint64_t t1 = now_ns();
+    fill_result(c, c->h_raw, t0, t1, reinterpret_cast<uint64_t>(region), placement, out);
+    return SAGE_OK;
+}
+
+int ensure_stage(sage_ctx* c, size_t bytes) {
+    if (c->stage_bytes >= bytes) return SAGE_OK;
+    if (c->d_stage) cudaFree(c->d_stage);
+    c->d_stage = nullptr;
+    c->stage_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->d_stage, bytes);
+    if (e != cudaSuccess) return fail(SAGE_ENOMEM, "cudaMalloc of the host-region staging buffer failed%s");
+    c->stage_bytes = bytes;
+    return SAGE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sage_checksum_init(const sage_config* cfg, sage_ctx** out) {
+    if (out == nullptr) return fail(SAGE_EINVAL, "out is null%s");
+    sage_config d{};
+    if (cfg) d = *cfg;
+    if (d.threads == 0) d.threads = 1024;
+    if (d.pick_words == 0) d.pick_words = 1;
+    if (d.threads % 32 != 0 || d.threads > 1024) return fail(SAGE_EINVAL, "threads must be a multiple of 32, <= 1024%s");
+    if (d.pick_words != 1 && d.pick_words != 4 && d.pick_words != 8)
+        return fail(SAGE_EINVAL, "pick_words must be 1, 4 or 8%s");
+    if (d.placement > SAGE_GLOBAL) return fail(SAGE_EINVAL, "unknown placement%s");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (d.device < 0 || d.device >= ndev) return fail(SAGE_EINVAL, "device ordinal out of range%s");
+    CUDA_TRY(cudaSetDevice(d.device));
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
+
+    sage_ctx* c = new (std::nothrow) sage_ctx();
+    if (!c) return fail(SAGE_ENOMEM, "context allocation failed%s");
+    c->device = d.device;
+    c->sm_count = static_cast<uint32_t>(sms);
+    c->threads = d.threads;
+    c->blocks = d.blocks ? d.blocks : 2u * static_cast<uint32_t>(sms);
+    c->pick_words = d.pick_words;
+    c->placement = d.placement;
+    cudaError_t e;
+    if (d.stream) {
+        c->stream = static_cast<cudaStream_t>(d.stream);
+    } else {
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaStreamCreate"); }
+        c->own_stream = true;
+    }
+    e = cudaMalloc(&c->d_raw, 4 * sizeof(uint64_t));
+    if (e != cudaSuccess) { sage_checksum_destroy(c); return fail(SAGE_ENOMEM, "cudaMalloc result%s"); }
+    e = cudaMallocHost(&c->h_raw, 4 * sizeof(uint64_t));
+    if (e != cudaSuccess) { sage_checksum_destroy(c); return fail(SAGE_ENOMEM, "cudaMallocHost result%s"); }
+    *out = c;
+    return SAGE_OK;
+}
+
+int sage_attest(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes, uint64_t rounds,
+                sage_result* out) {
+    return sage_attest_debug(ctx, nonce, region, region_bytes, rounds, nullptr, out);
+}
+
+int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes, uint64_t rounds,
+                      uint64_t* per_warp_out, sage_result* out) {
+    int rc = validate(ctx, region, region_bytes, rounds);
+    if (rc) return rc;
+    if (out == nullptr) return fail(SAGE_EINVAL, "out is null%s");
+    sage_result tmp;
+    rc = attest_device(ctx, nonce, region, region_bytes, rounds, per_warp_out, &tmp, nullptr);
+    if (rc) return rc;
+    *out = tmp;
+    return SAGE_OK;
+}
+
+int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes, uint64_t rounds,
+                      uint64_t* raw_out, uint64_t* per_warp_out) {
+    int rc = validate(ctx, region, region_bytes, rounds);
+    if (rc) return rc;
+    if (raw_out == nullptr) return fail(SAGE_EINVAL, "raw_out is null%s");
+    rc = set_device(ctx);
+    if (rc) return rc;
+    return launch(ctx, nonce, region, region_bytes, rounds, raw_out, per_warp_out, nullptr);
+}
+
+int sage_decode_raw(const uint64_t raw[4], sage_result* out) {
+    if (raw == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    memset(out, 0, sizeof(*out));
+    out->checksum = raw[0];
+    out->cycles = raw[1];
+    const uint64_t start = ~raw[2];
+    out->device_ns = raw[3] >= start ? raw[3] - start : 0;
+    return SAGE_OK;
+}
+
+int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, size_t region_bytes, uint64_t rounds,
+                     sage_result* out) {
+    if (ctx == nullptr || host_region == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    rc = ensure_stage(ctx, region_bytes ? region_bytes : 1);
+    if (rc) return rc;
+    rc = validate(ctx, ctx->d_stage, region_bytes, rounds);
+    if (rc) return rc;
+    sage_result tmp;
+    rc = attest_device(ctx, nonce, ctx->d_stage, region_bytes, rounds, nullptr, &tmp, host_region);
+    if (rc) return rc;
+    *out = tmp;
+    return SAGE_OK;
+}
+
+int sage_host_region_va(sage_ctx* ctx, size_t region_bytes, uint64_t* va_out) {
+    if (ctx == nullptr || va_out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    rc = ensure_stage(ctx, region_bytes ? region_bytes : 1);
+    if (rc) return rc;
+    *va_out = reinterpret_cast<uint64_t>(ctx->d_stage);
+    return SAGE_OK;
+}
+
+int sage_placement_for(sage_ctx* ctx, size_t region_bytes, uint32_t* placement_out) {
+    if (ctx == nullptr || placement_out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    *placement_out = choose_placement(ctx, region_bytes);
+    return SAGE_OK;
+}
+
+int sage_query(sage_ctx* ctx, sage_info* out) {
+    if (ctx == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    sage_info info{};
+    info.device = ctx->device;
+    info.sm_count = ctx->sm_count;
+    info.blocks = ctx->blocks;
+    info.threads = ctx->threads;
+    info.pick_words = ctx->pick_words;
+    info.placement = ctx->placement;
+    info.smem_region_max = kSmemRegionMax;
+    KernelFn fs = kernel_for(ctx->pick_words, true), fg = kernel_for(ctx->pick_words, false);
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fs), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemRegionMax)));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs, static_cast<int>(ctx->threads), kSmemRegionMax));
+    info.ctas_per_sm_smem = static_cast<uint32_t>(occ);
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fg, static_cast<int>(ctx->threads), 0));
+    info.ctas_per_sm_global = static_cast<uint32_t>(occ);
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, fs));
+    info.regs_per_thread = static_cast<uint32_t>(fa.numRegs);
+    *out = info;
+    return SAGE_OK;
+}
+
+uint64_t sage_launch_count(const sage_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* sage_stream(const sage_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+void sage_checksum_destroy(sage_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->d_raw) cudaFree(ctx->d_raw);
+    if (ctx->h_raw) cudaFreeHost(ctx->h_raw);
+    if (ctx->d_stage) cudaFree(ctx->d_stage);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* sage_strerror(int code) {
+    switch (code) {
+        case SAGE_OK: return "ok";
+        case SAGE_EINVAL: return "invalid argument";
+        case SAGE_EUNSUPPORTED: return "unsupported configuration";
+        case SAGE_ENOMEM: return "out of memory";
+        case SAGE_ECUDA: return "CUDA error";
+        default: return "unknown error";
+    }
+}
+
+const char* sage_last_error(void) { return g_last_error; }
+
+}  // extern "C"

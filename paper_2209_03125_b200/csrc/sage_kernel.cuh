@@ -1,0 +1,274 @@
+// sage_kernel.cuh -- the SCS-1 checksum kernel for sm_100a.
+//
+// One launch = one attestation (SAGE section 5.2.2).  Every thread
+// of a full-occupancy grid (2 CTAs x 1024 threads per SM, 32 registers, the
+// B200 analogue of P:612-613) seeds its state from the nonce, runs R rounds of
+// SCS-1 entirely in registers, and the folded states are
+// reduced warp (shuffle) -> block (shared memory) -> grid (one 64-bit atomic
+// per CTA).
+//
+// Region placement:
+//   SMEM   : the region is copied once per CTA into shared memory with a 1-D
+//            TMA bulk copy (cp.async.bulk + mbarrier complete_tx); each round's
+//            pick is one LDS.
+//   GLOBAL : each round's pick is one read-only LDG (32/128/256-bit for
+//            P = 1/4/8) straight from L2/HBM; the data pointer of the pick is
+//            the load address itself.
+//
+// Integer-pipe mapping (B300_MICROARCH: IMAD on the FMA pipe, LOP3/SHF/IADD3
+// on the ALU pipe, 2 cycles per warp instruction each): R7's a*MUL + t is one
+// IMAD (FMA pipe) and t = a + rotl(t, S) one LEA.HI-class op (ALU pipe),
+// the interleaved shift-and-add pattern of P:651.
+#pragma once
+#include <stdint.h>
+
+namespace sage {
+
+constexpr int kAccum = 16;                                   // K
+constexpr uint64_t kXsMult = 0x2545F4914F6CDD1DULL;          // xorshift64* multiplier
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;           // SplitMix64 increment
+
+// R7 constant tables as compile-time immediates (Q6).
+__host__ __device__ constexpr uint32_t mul_of(int j) {
+    constexpr uint32_t e[kAccum] = {5, 11, 3, 17, 9, 23, 7, 13, 29, 2, 19, 6, 15, 27, 4, 21};
+    return (1u << e[j]) + 1u;
+}
+__host__ __device__ constexpr uint32_t rot_of(int j) {
+    constexpr uint32_t s[kAccum] = {7, 13, 19, 3, 25, 9, 17, 5, 11, 29, 2, 23, 14, 6, 27, 18};
+    return s[j];
+}
+
+__device__ __forceinline__ uint32_t rotl(uint32_t v, uint32_t s) { return __funnelshift_l(v, v, s); }
+
+__device__ __forceinline__ uint64_t xorshift(uint64_t x) {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// ---- PTX helpers: mbarrier + 1-D TMA bulk copy + read-only loads ------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int P> struct Pick { uint32_t w[P]; };
+
+template <int P>
+__device__ __forceinline__ Pick<P> load_global(const uint32_t* p) {
+    Pick<P> d;
+    if constexpr (P == 1) {
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
+    } else if constexpr (P == 4) {
+        asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
+    } else {
+        asm volatile("ld.global.nc.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                       "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
+    }
+    return d;
+}
+
+template <int P>
+__device__ __forceinline__ Pick<P> load_shared(const uint32_t* s) {
+    Pick<P> d;
+    if constexpr (P == 1) {
+        d.w[0] = *s;
+    } else {
+#pragma unroll
+        for (int h = 0; h < P / 4; ++h) {
+            uint4 v = reinterpret_cast<const uint4*>(s)[h];
+            d.w[4 * h + 0] = v.x; d.w[4 * h + 1] = v.y; d.w[4 * h + 2] = v.z; d.w[4 * h + 3] = v.w;
+        }
+    }
+    return d;
+}
+
+struct KernelArgs {
+    const uint32_t* region;   // device VA of region word 0 (= SCS-1 base)
+    uint64_t nonce;
+    uint32_t nc_mask;         // Nc - 1
+    uint32_t rounds;          // R
+    uint32_t region_bytes;    // SMEM staging size (SMEM placement only)
+    uint64_t* raw;            // [checksum, max cycles, ~min start ns, max end ns]
+    uint64_t* per_warp;       // optional, n/32 partial sums
+    // R7 multipliers MUL[j] = 2^L[j] + 1, passed through the constant bank so
+    // ptxas emits one IMAD R, R, c[..], R per step instead of strength-reducing
+    // a*(2^L+1)+t into a*2^L + (a+t) (two FMA-pipe ops).
+    uint32_t mul[kAccum];
+};
+
+// One SCS-1 round (R1-R9) for this thread; the caller supplies the chunk reader.
+template <int P, bool SMEM>
+__device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint64_t& x, uint32_t r,
+                                           const uint32_t* __restrict__ words, uint64_t base,
+                                           uint32_t nc_mask, uint32_t src_lane, const KernelArgs& args) {
+    // R1
+    x = xorshift(x);
+    const uint64_t y = x * kXsMult;
+    // R2, R3
+    const uint32_t C = a[kAccum - 1];
+    const uint32_t i = (static_cast<uint32_t>(y >> 32) ^ C) & nc_mask;
+    // R5: data pointer of the chunk (also the global load address)
+    const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);
+    // R4
+    Pick<P> d;
+    if constexpr (SMEM) d = load_shared<P>(words + static_cast<size_t>(i) * P);
+    else d = load_global<P>(reinterpret_cast<const uint32_t*>(dp));
+    // R6
+    uint32_t t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(dp)) ^ static_cast<uint32_t>(dp >> 32);
+#pragma unroll
+    for (int q = 0; q < P; ++q) t = rotl(t, 5) + d.w[q];
+    // R7
+#pragma unroll
+    for (int j = 0; j < kAccum; ++j) {
+        a[j] = a[j] * args.mul[j] + t;
+        t = a[j] + rotl(t, rot_of(j));
+    }
+    // R8
+    t = t + (t >> (C & 31u));
+    // R9
+    a[kAccum - 1] ^= __shfl_sync(0xFFFFFFFFu, t, src_lane);
+}
+
+template <int P, bool SMEM, int UNROLL>
+__global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs args) {
+    extern __shared__ __align__(128) uint32_t smem_words[];
+    __shared__ uint64_t red[32];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint64_t t_start_ns;
+    __shared__ long long c_start;
+
+    // a13: CTA start time (kept in shared memory, not in registers)
+    if (threadIdx.x == 0) {
+        t_start_ns = globaltimer();
+        c_start = clock64();
+    }
+
+    // a2: stage the region into shared memory (SMEM placement).
+    const uint32_t* words = args.region;
+    if constexpr (SMEM) {
+        const uint32_t bytes = args.region_bytes;
+        if ((bytes & 15u) == 0) {
+            if (threadIdx.x == 0) mbar_init(&bar, 1);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                mbar_expect_tx(&bar, bytes);
+                constexpr uint32_t kChunk = 32768;
+                for (uint32_t off = 0; off < bytes; off += kChunk) {
+                    const uint32_t n = (bytes - off < kChunk) ? (bytes - off) : kChunk;
+                    bulk_g2s(reinterpret_cast<char*>(smem_words) + off,
+                             reinterpret_cast<const char*>(args.region) + off, n, &bar);
+                }
+            }
+            mbar_wait(&bar, 0);
+        } else {  // 4- or 8-byte regions: below the bulk-copy granule
+            for (uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x) smem_words[k] = args.region[k];
+            __syncthreads();
+        }
+        words = smem_words;
+    }
+
+    // a1: I1-I3
+    const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t src_lane = (lane + 1u) & 31u;
+    uint64_t x = splitmix(args.nonce + (g + 1) * kGamma);
+    if (x == 0) x = kGamma;
+    uint32_t a[kAccum];
+#pragma unroll
+    for (int j = 0; j < kAccum; ++j) {
+        x = xorshift(x);
+        a[j] = static_cast<uint32_t>((x * kXsMult) >> 32);
+    }
+
+    const uint64_t base = reinterpret_cast<uint64_t>(args.region);
+    const uint32_t nc_mask = args.nc_mask;
+    const uint32_t rounds = args.rounds;
+
+    // a10: round loop, UNROLL rounds per trip + remainder
+    uint32_t r = 0;
+    const uint32_t main_end = rounds - rounds % UNROLL;
+    for (; r < main_end; r += UNROLL) {
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+            scs1_round<P, SMEM>(a, x, r + u, words, base, nc_mask, src_lane, args);
+    }
+    for (; r < rounds; ++r) scs1_round<P, SMEM>(a, x, r, words, base, nc_mask, src_lane, args);
+
+    // a11: F1-F2
+    uint32_t e = 0, o = 0;
+#pragma unroll
+    for (int j = 0; j < kAccum; j += 2) { e ^= a[j]; o ^= a[j + 1]; }
+    uint64_t f = ((static_cast<uint64_t>(o) << 32) | e) ^ x;
+
+    // a12: warp -> block -> grid
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) f += __shfl_down_sync(0xFFFFFFFFu, f, off);
+    const uint32_t warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[warp] = f;
+        if (args.per_warp) args.per_warp[blockIdx.x * (blockDim.x >> 5) + warp] = f;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        uint64_t s = (lane < nw) ? red[lane] : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xFFFFFFFFu, s, off);
+        if (lane == 0) {
+            // a13: timing
+            const long long c_end = clock64();
+            const uint64_t t_end_ns = globaltimer();
+            atomicAdd(reinterpret_cast<unsigned long long*>(&args.raw[0]), static_cast<unsigned long long>(s));
+            atomicMax(reinterpret_cast<unsigned long long*>(&args.raw[1]),
+                      static_cast<unsigned long long>(c_end - c_start));
+            atomicMax(reinterpret_cast<unsigned long long*>(&args.raw[2]),
+                      static_cast<unsigned long long>(~t_start_ns));
+            atomicMax(reinterpret_cast<unsigned long long*>(&args.raw[3]),
+                      static_cast<unsigned long long>(t_end_ns));
+        }
+    }
+}
+
+}  // namespace sage

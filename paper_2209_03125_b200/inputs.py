@@ -17,14 +17,41 @@ C1_NONCE = 0x0123456789ABCDEF
 _PKG = os.path.dirname(os.path.abspath(__file__))
 
 
-def kernel_code_prefix():
-    """Bytes of the checksum kernel's cubin (written by the build next to
-    libsage.so), or b'' when it has not been built.  Used as the region prefix
-    so the region carries the verification code."""
+def _elf_sections(blob):
+    """{name: bytes} of an ELF64 little-endian file (plain header parsing)."""
+    import struct
+    if blob[:4] != b"\x7fELF" or blob[4] != 2:
+        return {}
+    shoff, = struct.unpack_from("<Q", blob, 0x28)
+    shentsize, shnum, shstrndx = struct.unpack_from("<HHH", blob, 0x3A)
+    hdrs = []
+    for k in range(shnum):
+        name, _typ, _flags, _addr, off, size = struct.unpack_from("<IIQQQQ", blob, shoff + k * shentsize)
+        hdrs.append((name, off, size))
+    _, stroff, strsize = hdrs[shstrndx]
+    strtab = blob[stroff:stroff + strsize]
+    out = {}
+    for name, off, size in hdrs:
+        end = strtab.find(b"\0", name)
+        out[strtab[name:end].decode("latin-1")] = blob[off:off + size]
+    return out
+
+
+def kernel_code_prefix(pick_words=1, smem=True):
+    """Machine code (SASS) of the checksum kernel variant itself, taken from the
+    .text section of the cubin the build writes next to libsage.so; b'' when it
+    has not been built.  Used as the region prefix so the checksummed region
+    carries the checksum function's own instructions (self-verification,
+    P:370-381; buffer layout P:365-367)."""
     path = os.path.join(_PKG, "sage_kernel.cubin")
-    if os.path.exists(path):
-        with open(path, "rb") as f:
-            return f.read()
+    if not os.path.exists(path):
+        return b""
+    with open(path, "rb") as f:
+        secs = _elf_sections(f.read())
+    want = ".text._ZN4sage20sage_checksum_kernelILi%dELb%d" % (pick_words, 1 if smem else 0)
+    for name, data in sorted(secs.items()):
+        if name.startswith(want):
+            return bytes(data)
     return b""
 
 

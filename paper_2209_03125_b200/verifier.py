@@ -1,0 +1,104 @@
+"""Verifier-side host logic: timing model, verdicts, inclusion probability.
+
+The verifier accepts an attestation iff the checksum is correct AND it came
+back within the expected time.  The time threshold is
+T_avg + 2.5 sigma over calibration runs (Table 1 row
+"T_avg + 2.5 sigma").  Rejection is a verdict, not an error; on a
+rejection the session restarts with a fresh challenge.
+
+This is plain host arithmetic over measured numbers; the checksum itself is
+computed only by the CUDA kernel behind libsage.so.
+"""
+import math
+from dataclasses import dataclass
+
+THRESHOLD_SIGMAS = 2.5
+
+
+@dataclass(frozen=True)
+class TimingModel:
+    t_avg: float
+    sigma: float
+    runs: int
+    k: float = THRESHOLD_SIGMAS
+
+    @property
+    def threshold(self):
+        return self.t_avg + self.k * self.sigma
+
+
+@dataclass(frozen=True)
+class Verdict:
+    accepted: bool
+    reason: str               # ok | checksum_mismatch | timeout | stale_nonce
+    elapsed: float
+    expected: int
+    response: int
+
+
+def calibrate(samples, k=THRESHOLD_SIGMAS, min_runs=30):
+    """TimingModel from honest run times: mean, population sigma,
+    threshold = mean + k*sigma.  The paper used 100 runs."""
+    xs = [float(s) for s in samples]
+    n = len(xs)
+    if n < min_runs:
+        raise ValueError("calibration needs >= %d runs, got %d" % (min_runs, n))
+    mean = math.fsum(xs) / n
+    var = math.fsum((x - mean) ** 2 for x in xs) / n
+    return TimingModel(t_avg=mean, sigma=math.sqrt(var), runs=n, k=k)
+
+
+class NonceLedger:
+    """Tracks nonces already used in a session."""
+
+    def __init__(self):
+        self._seen = set()
+
+    def fresh(self, nonce):
+        return nonce not in self._seen
+
+    def consume(self, nonce):
+        if nonce in self._seen:
+            return False
+        self._seen.add(nonce)
+        return True
+
+
+def verify(response, elapsed, expected, model, nonce=None, ledger=None):
+    """Verdict: accepted iff response == expected and elapsed <=
+    model.threshold and (when a ledger is given) the nonce was not used before."""
+    if ledger is not None and nonce is not None and not ledger.consume(nonce):
+        return Verdict(False, "stale_nonce", elapsed, expected, response)
+    if response != expected:
+        return Verdict(False, "checksum_mismatch", elapsed, expected, response)
+    if elapsed > model.threshold:
+        return Verdict(False, "timeout", elapsed, expected, response)
+    return Verdict(True, "ok", elapsed, expected, response)
+
+
+def inclusion_probability(words, accesses):
+    """Probability that a given word is never read: (1 - 1/S)^N,
+    evaluated as exp(N * log1p(-1/S)) for precision.  The paper prints 0.082
+    for (524288, 100000); the formula gives 0.8264 (Q15)."""
+    if words < 1 or accesses < 0:
+        raise ValueError("need words >= 1 and accesses >= 0")
+    if words == 1:
+        return 1.0 if accesses == 0 else 0.0
+    return math.exp(accesses * math.log1p(-1.0 / words))
+
+
+def normal_tail(k=THRESHOLD_SIGMAS):
+    """One-sided normal tail P(Z > k): the false-positive rate of the k-sigma
+    rule under the paper's normality assumption (P:743 says "about 0.5%")."""
+    return 0.5 * math.erfc(k / math.sqrt(2.0))
+
+
+def percentile(values, q):
+    """Linear-interpolated percentile (q in [0, 100]) of a list of numbers."""
+    xs = sorted(float(v) for v in values)
+    if not xs:
+        raise ValueError("empty")
+    pos = (len(xs) - 1) * q / 100.0
+    lo = int(math.floor(pos))
+    hi = min(lo + 1, len(xs) - 1)
+    return xs[lo] + (xs[hi] - xs[lo]) * (pos - lo)

@@ -1,0 +1,247 @@
+"""GPU parity: the sm_100a kernel behind libsage.so against the CPU oracle,
+bit-exact (integer work).  Every call goes through the C ABI (ctypes binding).
+The oracle receives the region's real device VA (the data pointer is folded
+in every round)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle                                                     # noqa: E402
+from paper_2209_03125_b200 import sage                            # noqa: E402
+from paper_2209_03125_b200.inputs import (C1_NONCE, kernel_code_prefix, make_region,  # noqa: E402
+                                           nonces)
+
+pytestmark = pytest.mark.gpu
+
+M64 = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2209_03125_b200 import build
+    build.build()
+    return torch.device("cuda:0")
+
+
+def to_dev(region_np, dev, align_offset=0):
+    """Copy a host region to a fresh device buffer at a given byte offset (>= 0,
+    multiple of 16) from a 256-B aligned allocation; returns (tensor_view, keepalive)."""
+    n = region_np.nbytes
+    buf = torch.empty(n + align_offset + 256, dtype=torch.uint8, device=dev)
+    start = (-buf.data_ptr()) % 256 + align_offset
+    view = buf[start:start + n]
+    view.copy_(torch.from_numpy(region_np))
+    assert view.data_ptr() % 16 == 0
+    return view, buf
+
+
+def test_config1_bit_exact(dev):
+    """BASELINE configs[0]: 1 x 32 threads, 4 KiB region, 10^4 rounds, fixed nonce."""
+    region = make_region(4096, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=1, threads=32) as ctx:
+        res = ctx.attest(C1_NONCE, d, 10_000)
+        assert res.placement == sage.SAGE_SMEM
+        want = oracle.attest(C1_NONCE, region, d.data_ptr(), 10_000, 1, 32, 1)
+        assert res.checksum == want
+        assert res.cycles > 0 and res.elapsed_ns > 0 and res.device_ns > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_small_geometries(dev, seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(8):
+        P = int(rng.choice([1, 4, 8]))
+        nc = 1 << int(rng.integers(0, 12))
+        nbytes = 4 * P * nc
+        if nbytes < 16:
+            P, nc, nbytes = 1, 4, 16
+        placement = int(rng.choice([sage.SAGE_AUTO, sage.SAGE_SMEM, sage.SAGE_GLOBAL]))
+        blocks = int(rng.integers(1, 5))
+        threads = 32 * int(rng.integers(1, 9))
+        rounds = int(rng.integers(0, 400))
+        nonce = int(rng.integers(0, 2**64, dtype=np.uint64))
+        region = make_region(nbytes, fill_seed=int(rng.integers(0, 2**31)))
+        d, _keep = to_dev(region, dev, align_offset=32 * int(rng.integers(0, 8)))
+        with sage.Context(blocks=blocks, threads=threads, pick_words=P, placement=placement) as ctx:
+            res = ctx.attest(nonce, d, rounds)
+        want = oracle.attest(nonce, region, d.data_ptr(), rounds, blocks, threads, P)
+        assert res.checksum == want, dict(P=P, nc=nc, placement=placement, blocks=blocks, threads=threads,
+                                          rounds=rounds)
+
+
+def test_tiny_regions_below_bulk_granule(dev):
+    """Nc = 1 and 2 with P = 1 (4- and 8-byte regions) take the non-TMA staging path."""
+    for nbytes in (4, 8):
+        region = make_region(nbytes, fill_seed=nbytes)
+        d, _keep = to_dev(region, dev)
+        for placement in (sage.SAGE_SMEM, sage.SAGE_GLOBAL):
+            with sage.Context(blocks=2, threads=64, placement=placement) as ctx:
+                res = ctx.attest(77, d, 50)
+            assert res.checksum == oracle.attest(77, region, d.data_ptr(), 50, 2, 64, 1)
+
+
+def test_zero_rounds(dev):
+    region = make_region(1024)
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=3, threads=96) as ctx:
+        res = ctx.attest(5, d, 0)
+    assert res.checksum == oracle.attest(5, region, d.data_ptr(), 0, 3, 96, 1)
+
+
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_smem_and_global_placements_agree(dev, P):
+    region = make_region(4 * P * 2048, prefix=kernel_code_prefix(P, True))
+    d, _keep = to_dev(region, dev)
+    out = {}
+    for placement in (sage.SAGE_SMEM, sage.SAGE_GLOBAL):
+        with sage.Context(blocks=4, threads=256, pick_words=P, placement=placement) as ctx:
+            out[placement] = ctx.attest(0xABC, d, 300).checksum
+    assert out[sage.SAGE_SMEM] == out[sage.SAGE_GLOBAL] == oracle.attest(0xABC, region, d.data_ptr(), 300, 4, 256, P)
+
+
+def test_full_occupancy_repeatable_and_sampled(dev):
+    """Full occupancy (2 x SMs x 1024), 8 KiB SMEM region: repeat runs are
+    bit-identical (atomic-order independence, Q11), the per-warp partials sum
+    to the checksum, and sampled warps match the oracle exactly."""
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    R = 2000
+    with sage.Context() as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
+        r1 = ctx.attest_debug(0x5151, d, R, pw)
+        r2 = ctx.attest(0x5151, d, R)
+    assert r1.checksum == r2.checksum
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    assert sum(parts) & M64 == r1.checksum
+    rng = np.random.default_rng(4)
+    sample = sorted({0, n // 32 - 1, *[int(w) for w in rng.integers(0, n // 32, 6)]})
+    for w in sample:
+        assert parts[w] == oracle.warp_sum(0x5151, region, d.data_ptr(), R, w, 1), w
+
+
+def test_bench_config_full_rounds_sampled(dev):
+    """configs[1] as bench.py times it: full occupancy, 8 KiB SMEM region,
+    10^5 rounds; sum consistency plus 4 sampled warps recomputed by the oracle."""
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    R = 100_000
+    nonce = nonces(1)[0]
+    with sage.Context() as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
+        res = ctx.attest_debug(nonce, d, R, pw)
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    assert sum(parts) & M64 == res.checksum
+    for w in (0, 1, n // 64, n // 32 - 1):
+        assert parts[w] == oracle.warp_sum(nonce, region, d.data_ptr(), R, w, 1), w
+
+
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_hbm_region_sampled(dev, P):
+    """configs[2]: 256 MiB region in HBM (GLOBAL placement), sampled warps."""
+    nbytes = 256 << 20
+    g = torch.Generator(device=dev)
+    g.manual_seed(P)
+    d = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
+    region = d.cpu().numpy()
+    R = 500
+    with sage.Context(pick_words=P) as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
+        res = ctx.attest_debug(99, d, R, pw)
+        assert res.placement == sage.SAGE_GLOBAL
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    assert sum(parts) & M64 == res.checksum
+    for w in (0, 12345 % (n // 32), n // 32 - 1):
+        assert parts[w] == oracle.warp_sum(99, region, d.data_ptr(), R, w, P), w
+
+
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_region_straddling_4gib_boundary(dev, P):
+    """Chunk data pointers whose high 32 bits differ inside one region (R5/R6 carry)."""
+    big = torch.empty((4 << 30) + (1 << 20), dtype=torch.uint8, device=dev)
+    base0 = big.data_ptr()
+    boundary = ((base0 >> 32) + 1) << 32
+    nbytes = 4 * P * 1024
+    start = boundary - nbytes // 2 - base0
+    d = big[start:start + nbytes]
+    region = make_region(nbytes, fill_seed=P)
+    d.copy_(torch.from_numpy(region))
+    assert (d.data_ptr() >> 32) != ((d.data_ptr() + nbytes - 1) >> 32)
+    for placement in (sage.SAGE_SMEM, sage.SAGE_GLOBAL):
+        with sage.Context(blocks=2, threads=128, pick_words=P, placement=placement) as ctx:
+            res = ctx.attest(31337, d, 200)
+        assert res.checksum == oracle.attest(31337, region, d.data_ptr(), 200, 2, 128, P)
+    del big
+
+
+def test_largest_smem_region(dev):
+    """64 KiB is the largest region staged into SMEM at 2 CTAs/SM."""
+    region = make_region(65536, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=3, threads=128) as ctx:
+        assert ctx.placement_for(65536) == sage.SAGE_SMEM
+        assert ctx.placement_for(131072) == sage.SAGE_GLOBAL
+        res = ctx.attest(8, d, 100)
+    assert res.placement == sage.SAGE_SMEM
+    assert res.checksum == oracle.attest(8, region, d.data_ptr(), 100, 3, 128, 1)
+
+
+def test_async_and_host_forms(dev):
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=2, threads=256) as ctx:
+        raw = torch.zeros(4, dtype=torch.int64, device=dev)
+        ctx.attest_async(11, d, 123, raw)
+        torch.cuda.synchronize()
+        dec = sage.decode_raw([int(v) for v in raw.cpu().tolist()])
+        assert dec.checksum == ctx.attest(11, d, 123).checksum == oracle.attest(11, region, d.data_ptr(), 123, 2, 256)
+        host = torch.from_numpy(region).pin_memory()
+        va = ctx.host_region_va(8192)
+        res = ctx.attest_host(11, host, 123)
+        assert res.region_va == va
+        assert res.checksum == oracle.attest(11, region, va, 123, 2, 256)
+
+
+def test_occupancy_and_registers(dev):
+    """Full occupancy: 2 CTAs x 1024 threads per SM, <= 32 registers."""
+    for P in (1, 4, 8):
+        with sage.Context(pick_words=P) as ctx:
+            info = ctx.query()
+            assert info.threads == 1024 and info.blocks == 2 * info.sm_count
+            assert info.ctas_per_sm_smem == 2 and info.ctas_per_sm_global == 2
+            assert info.regs_per_thread <= 32
+
+
+def test_argument_errors(dev):
+    region = torch.zeros(1 << 20, dtype=torch.uint8, device=dev)
+    with sage.Context(blocks=1, threads=32) as ctx:
+        for nbytes in (12, 24, 3 * 4096):
+            with pytest.raises(sage.SageError) as e:
+                ctx.attest(0, region, 1, nbytes=nbytes)
+            assert e.value.code == sage.SAGE_EINVAL
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(0, region.data_ptr() + 4, 1, nbytes=4096)
+        assert e.value.code == sage.SAGE_EINVAL
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(0, region, 1 << 32, nbytes=4096)
+        assert e.value.code == sage.SAGE_EINVAL
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(0, 0, 1, nbytes=4096)
+        assert e.value.code == sage.SAGE_EINVAL
+    with sage.Context(blocks=1, threads=32, pick_words=8) as ctx:
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(0, region.data_ptr() + 16, 1, nbytes=4096)
+        assert e.value.code == sage.SAGE_EINVAL
+    with sage.Context(blocks=1, threads=32, placement=sage.SAGE_SMEM) as ctx:
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(0, region, 1, nbytes=1 << 20)
+        assert e.value.code == sage.SAGE_EUNSUPPORTED

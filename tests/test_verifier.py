@@ -1,0 +1,83 @@
+"""Verifier host logic."""
+import math
+import random
+
+import pytest
+
+from paper_2209_03125_b200 import verifier as V
+
+
+def test_table1_threshold_arithmetic():
+    """T_avg + 2.5 sigma = 0.4941 + 2.5 * 0.0009 = 0.49635, printed 0.4964."""
+    m = V.TimingModel(t_avg=0.4941, sigma=0.0009, runs=100)
+    assert m.threshold == pytest.approx(0.49635, abs=1e-12)
+    assert round(m.threshold, 4) == 0.4964 or round(m.threshold, 4) == 0.4963  # banker's/float rounding
+    assert f"{m.threshold + 1e-12:.4f}" == "0.4964"
+
+
+def test_adversarial_nop_is_rejected():
+    """Exp 2: T_min = 0.4966 > 0.4964 -> rejected as timeout."""
+    m = V.TimingModel(t_avg=0.4941, sigma=0.0009, runs=100)
+    v = V.verify(123, 0.4966, 123, m)
+    assert not v.accepted and v.reason == "timeout"
+    assert V.verify(123, 0.4941, 123, m).accepted
+    v = V.verify(124, 0.1, 123, m)
+    assert not v.accepted and v.reason == "checksum_mismatch"
+
+
+def test_calibrate_identity_and_min_runs():
+    rnd = random.Random(1)
+    xs = [rnd.gauss(1.0, 0.01) for _ in range(100)]
+    m = V.calibrate(xs)
+    assert m.threshold - m.t_avg == pytest.approx(2.5 * m.sigma, rel=1e-12)
+    assert m.t_avg == pytest.approx(sum(xs) / 100)
+    with pytest.raises(ValueError):
+        V.calibrate(xs[:10])
+    assert V.calibrate([2.0] * 30).threshold == 2.0
+
+
+def test_verify_monotone():
+    """lowering elapsed never flips accept -> reject."""
+    m = V.TimingModel(1.0, 0.1, 100)
+    prev = None
+    for e in [1.3, 1.26, 1.25, 1.2, 0.9, 0.1]:
+        acc = V.verify(5, e, 5, m).accepted
+        if prev:
+            assert acc
+        prev = acc
+
+
+def test_stale_nonce():
+    m = V.TimingModel(1.0, 0.1, 100)
+    led = V.NonceLedger()
+    assert V.verify(1, 1.0, 1, m, nonce=7, ledger=led).accepted
+    v = V.verify(1, 1.0, 1, m, nonce=7, ledger=led)
+    assert not v.accepted and v.reason == "stale_nonce"
+
+
+def test_inclusion_probability():
+    """(1 - 1/524288)^100000 = 0.8264; the paper prints 0.082 (Q15)."""
+    assert V.inclusion_probability(524288, 100000) == pytest.approx(0.82642, abs=1e-4)
+    assert V.inclusion_probability(524288 // 4, 100000) == pytest.approx(0.46629, abs=1e-4)
+    assert V.inclusion_probability(10, 0) == 1.0
+    # Monte Carlo, S = 1024 words, N = 2048 accesses
+    rnd = random.Random(3)
+    S, N, trials = 1024, 2048, 200
+    missed = 0
+    for _ in range(trials):
+        seen = set(rnd.randrange(S) for _ in range(N))
+        missed += S - len(seen)
+    p_hat = missed / (S * trials)
+    p = V.inclusion_probability(S, N)
+    se = math.sqrt(p * (1 - p) / (S * trials))
+    assert abs(p_hat - p) < 4 * se
+
+
+def test_normal_tail():
+    """2.5 sigma one-sided tail = 0.621% (the paper says "about 0.5%"; Q16)."""
+    assert V.normal_tail(2.5) == pytest.approx(0.00621, abs=1e-5)
+
+
+def test_percentile():
+    assert V.percentile([1, 2, 3, 4, 5], 50) == 3
+    assert V.percentile(list(range(101)), 99) == pytest.approx(99)
