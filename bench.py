@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py -- SAGE checksum hot path on B200 (arXiv 2209.03125).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2a] [--impl ours|reference]
+
+A step is one attestation: one launch of the checksum kernel over the whole
+grid (all SURVEY 8(a) rows: seeding, staging, R rounds, fold, reduction,
+timing).  N=1 workload = BASELINE.json configs[1]: full occupancy
+(2 x SMs x 1024 threads), 8 KiB SMEM-resident region = the checksum kernel's
+own machine code (+ PCG64 fill if shorter), R = 10^5 rounds (Exp 1).
+For N > 1 (torchrun) every GPU runs an independent replica with its own
+nonce (attestation is per-GPU); results are gathered to rank 0.
+
+Prints one JSON line (rank 0).  value = whole-job thread-rounds/s (sum over
+ranks of n*R*K / max-over-ranks bracketed time).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "checksum rounds/s and checksummed GB/s per B200 (1/2/4/8 GPU); p99 attest time"
+UNIT = "thread-rounds/s"
+
+# Algorithmic 32-bit integer operations per thread-round of SCS-1 (DESIGN.md
+# section 7): minimal sm_100 lowering with 3-input LOP3 / IMAD / LEA.HI.
+OPS_PER_ROUND = {1: 59, 4: 62, 8: 67}
+
+CONFIGS = {
+    # name: (region bytes, P, rounds, description)
+    "c1": (4096, 1, 10_000, "1 block x 32 threads, 4 KiB SMEM region, 1e4 rounds"),
+    "c2a": (8192, 1, 100_000, "full occupancy, 8 KiB SMEM region (kernel code), 1e5 rounds"),
+    "c2b": (65536, 1, 100_000, "full occupancy, 64 KiB SMEM region, 1e5 rounds"),
+    "c2c": (524288, 1, 100_000, "full occupancy, 512 KiB region in L2 (GLOBAL), 1e5 rounds"),
+    "c3p1": (256 << 20, 1, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=1, 1e4 rounds"),
+    "c3p4": (256 << 20, 4, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=4, 1e4 rounds"),
+    "c3p8": (256 << 20, 8, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=8, 1e4 rounds"),
+}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_traffic(workload):
+    """dram bytes per launch from the committed ncu --set full summary, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            ent = json.load(f).get(workload)
+        if isinstance(ent, dict):
+            return ent.get("dram_bytes_per_launch")
+        return ent
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        busy = [v for v in sm if smax and v > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------------- oracle arm
+def cpu_oracle_rate(region, base, rounds, warps, P, workers):
+    """Time the oracle (as it stands) on `warps` warps over host cores."""
+    import oracle
+    t0 = time.perf_counter()
+    sums = oracle.warp_sums_parallel(0x1234, region, base, rounds, warps, P, workers=workers)
+    dt = time.perf_counter() - t0
+    return len(warps) * 32 * rounds / dt, dt, sums
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+    import oracle
+    from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region
+    nbytes, P, R, desc = CONFIGS[args.config]
+    oracle.build()
+    region = make_region(nbytes, prefix=kernel_code_prefix(P, nbytes <= 65536)) if nbytes <= (1 << 20) else \
+        make_region(nbytes)
+    cores = len(os.sched_getaffinity(0))
+    base = 0x7F00_0000_0000
+    sample_warps = list(range(4 * cores))
+    times = []
+    for k in range(args.warmup + args.steps):
+        rate, dt, _ = cpu_oracle_rate(region, base, R, sample_warps, P, cores)
+        if k >= args.warmup:
+            times.append(dt)
+    tr = len(sample_warps) * 32 * R
+    value = tr * len(times) / sum(times)
+    sample = "%d warps (%d threads) x %d rounds per step, %s" % (len(sample_warps), 32 * len(sample_warps), R,
+                                                                 desc)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": {"workload": args.config, "desc": desc, "region_bytes": nbytes, "P": P,
+                                              "rounds": R},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_03125_b200 import build, sage
+    from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces
+
+    ws, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        build.build()
+    if ws > 1:
+        dist.barrier()
+
+    nbytes, P, R, desc = CONFIGS[args.config]
+    if args.rounds:
+        R = args.rounds
+    smem = nbytes <= 65536
+    if nbytes <= (1 << 20):
+        region_np = make_region(nbytes, prefix=kernel_code_prefix(P, smem))
+        region = torch.from_numpy(region_np).to(dev)
+    else:
+        region_np = None
+        g = torch.Generator(device=dev)
+        g.manual_seed(0x5EED0001)
+        region = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    blocks, threads = (1, 32) if args.config == "c1" else (0, 0)
+    ctx = sage.Context(device=local, blocks=blocks, threads=threads, pick_words=P, stream=stream)
+    info = ctx.query()
+    n = info.blocks * info.threads
+    placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
+    my_nonces = nonces(args.warmup + args.steps + 64, master_seed=0x220903125 + rank)
+    total = args.warmup + args.steps
+    raw = torch.zeros(total, 4, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(total)]
+
+    for k in range(args.warmup):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        ctx.attest_async(my_nonces[k], region, R, raw[k])
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = ctx.launches
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for k in range(args.warmup, total):
+        flush.fill_(k & 0xFF)                                 # L2 flush between timed steps
+        ev[k][0].record(stream)
+        ctx.attest_async(my_nonces[k], region, R, raw[k])
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    launches = ctx.launches - launches0
+    kern_s = [ev[k][0].elapsed_time(ev[k][1]) / 1e3 for k in range(args.warmup, total)]
+    # the bracket, max over ranks
+    t_bracket = torch.tensor([t_wall], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_bracket, op=dist.ReduceOp.MAX)
+    t_bracket = float(t_bracket.item())
+    raws = raw.cpu().tolist()
+    dec = [sage.decode_raw(r) for r in raws[args.warmup:]]
+
+    # e2e through the public C API with HOST buffers (pinned): H2D of the
+    # region + kernel + D2H of the 32-byte result, every step.
+    host_region = torch.from_numpy(region_np).pin_memory() if region_np is not None else None
+    e2e = None
+    if host_region is not None:
+        ctx_h = sage.Context(device=local, blocks=blocks, threads=threads, pick_words=P, stream=stream)
+        for k in range(min(2, args.warmup)):
+            ctx_h.attest_host(my_nonces[k], host_region, R)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_ns = []
+        for k in range(args.steps):
+            r = ctx_h.attest_host(my_nonces[args.warmup + k], host_region, R)
+            e2e_ns.append(r.elapsed_ns)
+        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * n * R * args.steps / float(t_e2e.item()), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32,
+               "api": "sage_attest_host (pinned host region)"}
+        ctx_h.close()
+
+    # attestation wall time as the verifier sees it (sage_attest, device region)
+    att = []
+    for k in range(args.steps):
+        r = ctx.attest(my_nonces[total + (k % 64)], region, R)
+        att.append(r.elapsed_ns / 1e6)
+
+    # per-warp partials of one attestation, for the sampled parity check below
+    pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
+    dbg = ctx.attest_debug(0x1234, region, R, pw)
+    parts = [int(v) & (2**64 - 1) for v in pw.cpu().tolist()]
+
+    # gather per-replica results to rank 0 (the only cross-GPU step, 8(e))
+    mine = {"rank": rank, "checksum": "0x%016x" % dec[-1].checksum, "cycles": dec[-1].cycles,
+            "device_ns": dec[-1].device_ns, "kernel_ms_mean": 1e3 * statistics.mean(kern_s)}
+    if ws > 1:
+        allr = [None] * ws
+        dist.all_gather_object(allr, mine)
+    else:
+        allr = [mine]
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        mean_k = statistics.mean(kern_s)
+        value = ws * n * R * args.steps / t_bracket
+        ops = OPS_PER_ROUND[P]
+        f_clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        sms = info.sm_count
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * t_bracket / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": {"workload": args.config, "desc": desc, "region_bytes": nbytes, "P": P, "rounds": R,
+                           "blocks": info.blocks, "threads": info.threads, "threads_total": n,
+                           "placement": placement, "parallelism": "replica x%d" % ws,
+                           "l2": "256 MiB buffer written between timed steps (flush)"},
+                "checksummed_gbps": value * 4 * P / 1e9,
+                "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(kern_s), "max": 1e3 * max(kern_s)},
+                "attest_ms": {"p50": statistics.median(att), "p99": _pct(att, 99), "mean": statistics.mean(att),
+                              "sigma": statistics.pstdev(att), "threshold_2p5sigma":
+                              statistics.mean(att) + 2.5 * statistics.pstdev(att), "n": len(att)},
+                "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
+        if placement == "global" and nbytes > (1 << 20):
+            achieved = n * R * 32.0 / mean_k / 1e9       # DRAM sectors touched (one 32-B sector per pick)
+            line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic(args.config),
+                                "peak_source": peak_src + " hbm_gbs (copy)",
+                                "achieved_def": "one 32-B DRAM sector per pick x n x R / kernel time"}
+        else:
+            peak_ops = sms * 4 * 32 * f_clk / 1e12
+            achieved = n * R * ops / mean_k / 1e12
+            line["roofline"] = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
+                                "frac": achieved / peak_ops, "traffic": load_traffic(args.config),
+                                "peak_source": "%d SMs x 4 SMSP x 32 lanes x 1 issue/clk x %s sm_max_mhz %.0f "
+                                               "(DESIGN.md 7)" % (sms, peak_src, f_clk / 1e6),
+                                "ops_per_thread_round": ops}
+        if ws > 1:
+            line["replicas"] = allr
+        if ws == 1 and not args.no_cpu_baseline:
+            import oracle
+            oracle.build()
+            cores = len(os.sched_getaffinity(0))
+            host = region_np if region_np is not None else region.cpu().numpy()
+            nw = n // 32
+            want = min(nw, 32 * cores)
+            sample = sorted(set(int(round(i * (nw - 1) / max(1, want - 1))) for i in range(want)))
+            rate, dt, sums = cpu_oracle_rate(host, region.data_ptr(), R, sample, P, cores)
+            ok = all(sums[w] == parts[w] for w in sample) and (sum(parts) & (2**64 - 1)) == dbg.checksum
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": "%d warps x %d threads x %d rounds of this workload (%.1f s)"
+                                              % (len(sample), 32, R, dt),
+                                    "parity_on_sample": ok}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _pct(xs, q):
+    s = sorted(xs)
+    pos = (len(s) - 1) * q / 100.0
+    lo = int(math.floor(pos))
+    hi = min(lo + 1, len(s) - 1)
+    return s[lo] + (s[hi] - s[lo]) * (pos - lo)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2a", choices=sorted(CONFIGS))
+    ap.add_argument("--rounds", type=int, default=0, help="override the workload's round count")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

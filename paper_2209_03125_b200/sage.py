@@ -126,8 +126,20 @@ def _nbytes(buf, nbytes):
 
 
 # ---- the C entry points, one Python function each -------------------------------------
+def _stream_handle(stream):
+    """cudaStream_t from a torch.cuda.Stream, an int handle or None (ctx-owned).
+    Handle 0 (torch's legacy default stream) is refused: the library would read
+    it as NULL and launch on its own stream, unordered with the caller's work."""
+    if stream is None:
+        return None
+    h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    if h == 0:
+        raise ValueError("pass a non-default stream (e.g. torch.cuda.Stream()); handle 0 means ctx-owned")
+    return h
+
+
 def checksum_init(device=0, blocks=0, threads=0, pick_words=1, placement=SAGE_AUTO, stream=None):
-    cfg = sage_config(device, blocks, threads, pick_words, placement, stream)
+    cfg = sage_config(device, blocks, threads, pick_words, placement, _stream_handle(stream))
     ctx = ctypes.c_void_p()
     _check(load().sage_checksum_init(ctypes.byref(cfg), ctypes.byref(ctx)))
     return ctx

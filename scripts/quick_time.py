@@ -18,7 +18,8 @@ def time_cfg(nbytes, P, R, reps=5, placement=sage.SAGE_AUTO):
         region = torch.from_numpy(make_region(nbytes, prefix=kernel_code_prefix(P, True))).to(dev)
     else:
         region = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev)
-    s = torch.cuda.current_stream()
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
     with sage.Context(pick_words=P, placement=placement, stream=s.cuda_stream) as ctx:
         info = ctx.query()
         n = info.blocks * info.threads
