@@ -1,0 +1,99 @@
+// variants.cu -- development harness: times lowering variants of the SCS-1
+// kernel (sage_kernel.cuh) at full occupancy on one SMEM/GLOBAL workload and
+// checks they all return the same checksum.  Not part of the product path.
+//
+//   ./variants [rounds] [region_bytes]
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "sage_kernel.cuh"
+
+#define CK(x)                                                                  \
+    do {                                                                       \
+        cudaError_t e = (x);                                                   \
+        if (e != cudaSuccess) {                                                \
+            fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e));            \
+            exit(1);                                                           \
+        }                                                                      \
+    } while (0)
+
+using Fn = void (*)(const sage::KernelArgs);
+struct V { const char* name; Fn fn; int P; bool smem; bool straddle; };
+
+#define VAR(P, S, ST, XS, U) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U, \
+                              sage::sage_checksum_kernel<P, S, ST, XS, U>, P, S, ST}
+#define VARL(P, LD) {"P" #P " global ld" #LD, sage::sage_checksum_kernel<P, false, true, 0, 1, 0, LD>, P, false, true}
+#define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
+                              sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
+
+static V variants[] = {
+    VAR(1, true, false, 0, 1), VARA(1, true, false, 0, 1, 1), VARA(1, true, false, 0, 2, 1),
+    VAR(4, true, false, 0, 1), VARA(4, true, false, 0, 1, 1), VAR(8, true, false, 0, 1), VARA(8, true, false, 0, 1, 1),
+    VARL(1, 0), VARL(1, 1), VARL(1, 2), VARL(4, 0), VARL(4, 1), VARL(4, 2), VARL(8, 0), VARL(8, 1), VARL(8, 2),
+};
+
+int main(int argc, char** argv) {
+    const uint32_t rounds = argc > 1 ? atoi(argv[1]) : 100000;
+    const size_t bytes = argc > 2 ? strtoull(argv[2], nullptr, 10) : 8192;
+    const int gran = argc > 3 ? atoi(argv[3]) : -1;
+    size_t cur = 0;
+    CK(cudaDeviceGetLimit(&cur, cudaLimitMaxL2FetchGranularity));
+    if (gran >= 0) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran));
+    size_t now = 0;
+    CK(cudaDeviceGetLimit(&now, cudaLimitMaxL2FetchGranularity));
+    fprintf(stderr, "L2 fetch granularity default %zu now %zu\n", cur, now);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int blocks = 2 * sms, threads = 1024;
+    std::vector<uint8_t> h(bytes);
+    srand(7);
+    for (auto& b : h) b = rand() & 0xFF;
+    uint8_t* d = nullptr;
+    CK(cudaMalloc(&d, bytes));
+    CK(cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice));
+    uint64_t* raw = nullptr;
+    CK(cudaMalloc(&raw, 32));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const bool straddles = (reinterpret_cast<uint64_t>(d) >> 32) != ((reinterpret_cast<uint64_t>(d) + bytes - 1) >> 32);
+    unsigned long long ref[9] = {0};
+    for (auto& v : variants) {
+        if (!v.straddle && straddles) continue;
+        if (v.smem && bytes > 65536) continue;
+        if (v.smem) CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        sage::KernelArgs a{};
+        a.region = reinterpret_cast<const uint32_t*>(d);
+        a.nonce = 0x1234;
+        a.nc_mask = uint32_t(bytes / (4 * v.P) - 1);
+        a.rounds = rounds;
+        a.region_bytes = v.smem ? uint32_t(bytes) : 0;
+        a.raw = raw;
+        sage::fill_tables(a, v.P);
+        float best = 1e30f;
+        unsigned long long h_raw[4];
+        for (int rep = 0; rep < 3; ++rep) {
+            CK(cudaMemset(raw, 0, 32));
+            CK(cudaEventRecord(e0));
+            v.fn<<<blocks, threads, v.smem ? bytes : 0>>>(a);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaGetLastError());
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            if (ms < best) best = ms;
+            CK(cudaMemcpy(h_raw, raw, 32, cudaMemcpyDeviceToHost));
+        }
+        if (ref[v.P] == 0) ref[v.P] = h_raw[0];
+        const double tr = double(blocks) * threads * rounds / (best * 1e-3);
+        printf("{\"variant\": \"%s\", \"ms\": %.3f, \"thread_rounds_per_s\": %.4e, \"cycles\": %llu, "
+               "\"cycles_per_round\": %.1f, \"checksum\": \"0x%016llx\", \"same\": %s}\n",
+               v.name, best, tr, h_raw[1], double(h_raw[1]) / rounds, h_raw[0], h_raw[0] == ref[v.P] ? "true" : "false");
+        fflush(stdout);
+    }
+    return 0;
+}

@@ -39,19 +39,28 @@ uint64_t now_ns() {
     return static_cast<uint64_t>(ts.tv_sec) * 1000000000ull + static_cast<uint64_t>(ts.tv_nsec);
 }
 
-#ifndef SAGE_UNROLL
-#define SAGE_UNROLL 1
-#endif
-constexpr int kUnroll = SAGE_UNROLL;
 constexpr size_t kSmemRegionMax = 64 * 1024;   // 2 CTAs/SM x 64 KiB fits the 228 KB SM
 
 using KernelFn = void (*)(const sage::KernelArgs);
 
-KernelFn kernel_for(uint32_t P, bool smem) {
+// Kernel variant per (P, placement, straddle).  Lowering choices measured on
+// B200 with bench/variants.cu: SMEM picks address
+// shared memory through an IMAD (ADDR=1) unless chunk addresses straddle a
+// 4 GiB boundary; GLOBAL picks use L1-allocating read-only loads.
+template <int P>
+KernelFn kernel_for_p(bool smem, bool straddle) {
+    if (smem) {
+        return straddle ? sage::sage_checksum_kernel<P, true, true, 0, 1, 0, 0>
+                        : sage::sage_checksum_kernel<P, true, false, 0, 1, 1, 0>;
+    }
+    return sage::sage_checksum_kernel<P, false, true, 0, 1, 0, 0>;
+}
+
+KernelFn kernel_for(uint32_t P, bool smem, bool straddle) {
     switch (P) {
-        case 1: return smem ? sage::sage_checksum_kernel<1, true, kUnroll> : sage::sage_checksum_kernel<1, false, kUnroll>;
-        case 4: return smem ? sage::sage_checksum_kernel<4, true, kUnroll> : sage::sage_checksum_kernel<4, false, kUnroll>;
-        case 8: return smem ? sage::sage_checksum_kernel<8, true, kUnroll> : sage::sage_checksum_kernel<8, false, kUnroll>;
+        case 1: return kernel_for_p<1>(smem, straddle);
+        case 4: return kernel_for_p<4>(smem, straddle);
+        case 8: return kernel_for_p<8>(smem, straddle);
         default: return nullptr;
     }
 }
@@ -95,8 +104,12 @@ int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t round
     return SAGE_OK;
 }
 
+// SAGE_AUTO: SMEM when the region fits at 2 CTAs/SM, except P = 8, whose
+// random 32-B picks conflict heavily in shared-memory banks and run faster
+// from L1 (measured: 1510 vs 1843 cycles per round at 8 KiB).
 uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
     if (c->placement != SAGE_AUTO) return c->placement;
+    if (c->pick_words == 8) return SAGE_GLOBAL;
     return bytes <= kSmemRegionMax ? SAGE_SMEM : SAGE_GLOBAL;
 }
 
@@ -106,7 +119,9 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     if (placement == SAGE_SMEM && bytes > kSmemRegionMax)
         return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s", "64 KiB");
     const bool smem = placement == SAGE_SMEM;
-    KernelFn fn = kernel_for(c->pick_words, smem);
+    const uint64_t lo = reinterpret_cast<uint64_t>(region);
+    const bool straddle = (lo >> 32) != ((lo + bytes - 1) >> 32);
+    KernelFn fn = kernel_for(c->pick_words, smem, straddle);
     const size_t dyn = smem ? bytes : 0;
     if (smem) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
@@ -118,7 +133,7 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     args.region_bytes = static_cast<uint32_t>(smem ? bytes : 0);
     args.raw = raw;
     args.per_warp = per_warp;
-    for (int j = 0; j < sage::kAccum; ++j) args.mul[j] = sage::mul_of(j);
+    sage::fill_tables(args, c->pick_words);
     fn<<<c->blocks, c->threads, dyn, c->stream>>>(args);
     CUDA_TRY(cudaGetLastError());
     c->launches++;
@@ -292,7 +307,7 @@ int sage_query(sage_ctx* ctx, sage_info* out) {
     info.pick_words = ctx->pick_words;
     info.placement = ctx->placement;
     info.smem_region_max = kSmemRegionMax;
-    KernelFn fs = kernel_for(ctx->pick_words, true), fg = kernel_for(ctx->pick_words, false);
+    KernelFn fs = kernel_for(ctx->pick_words, true, false), fg = kernel_for(ctx->pick_words, false, true);
     CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fs), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemRegionMax)));
     int occ = 0;

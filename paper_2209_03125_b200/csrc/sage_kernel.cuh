@@ -93,18 +93,40 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 template <int P> struct Pick { uint32_t w[P]; };
 
-template <int P>
+// Read-only global loads of one P-word chunk.  LD selects the cache policy:
+//   0: ld.global.nc                      (L1-allocating; small, L1-resident regions)
+//   1: ld.global.nc.L1::no_allocate      (sector-granular L2 requests; L2/HBM regions)
+//   2: ld.global.cg                      (cache at L2 only)
+template <int P, int LD>
 __device__ __forceinline__ Pick<P> load_global(const uint32_t* p) {
     Pick<P> d;
     if constexpr (P == 1) {
-        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
+        if constexpr (LD == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
+        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
+        else asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
     } else if constexpr (P == 4) {
-        asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
+        if constexpr (LD == 0)
+            asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
+        else if constexpr (LD == 1)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
+        else
+            asm volatile("ld.global.cg.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
     } else {
-        asm volatile("ld.global.nc.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
-                       "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
+        if constexpr (LD == 0)
+            asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
+        else if constexpr (LD == 1)
+            asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
+        else
+            asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
     }
     return d;
 }
@@ -124,6 +146,21 @@ __device__ __forceinline__ Pick<P> load_shared(const uint32_t* s) {
     return d;
 }
 
+template <int P>
+__device__ __forceinline__ Pick<P> load_shared_addr(uint32_t addr) {
+    Pick<P> d;
+    if constexpr (P == 1) {
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(d.w[0]) : "r"(addr));
+    } else {
+#pragma unroll
+        for (int h = 0; h < P / 4; ++h)
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(d.w[4 * h]), "=r"(d.w[4 * h + 1]), "=r"(d.w[4 * h + 2]), "=r"(d.w[4 * h + 3])
+                         : "r"(addr + 16 * h));
+    }
+    return d;
+}
+
 struct KernelArgs {
     const uint32_t* region;   // device VA of region word 0 (= SCS-1 base)
     uint64_t nonce;
@@ -136,27 +173,93 @@ struct KernelArgs {
     // ptxas emits one IMAD R, R, c[..], R per step instead of strength-reducing
     // a*(2^L+1)+t into a*2^L + (a+t) (two FMA-pipe ops).
     uint32_t mul[kAccum];
+    // 2^20, 2^25, 2^5: xorshift shift multipliers for the IMAD.WIDE lowering
+    // (constant bank, so ptxas cannot turn them back into ALU shifts).
+    uint32_t p2[3];
+    uint32_t four_p;          // 4*P as a runtime value (forces IMAD for the chunk offset)
 };
 
-// One SCS-1 round (R1-R9) for this thread; the caller supplies the chunk reader.
-template <int P, bool SMEM>
-__device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint64_t& x, uint32_t r,
-                                           const uint32_t* __restrict__ words, uint64_t base,
-                                           uint32_t nc_mask, uint32_t src_lane, const KernelArgs& args) {
+// The region staged in shared memory (SMEM placement): namespace-scope so the
+// round can address it with a constant base (LDS [v + const]).
+extern __shared__ __align__(128) uint32_t smem_words[];
+
+// R1 state step with a selectable lowering of each 64-bit shift-xor.
+// XS bit k set => step k uses IMAD.WIDE.U32 by 2^s on the FMA pipe to
+// produce both 32-bit halves of the cross-word shift, instead of the funnel
+// shift on the ALU pipe.  Same function either way (xorshift64 (12,25,27)).
+template <int XS>
+__device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const KernelArgs& args) {
+    // x ^= x >> 12
+    if constexpr (XS & 8) {
+        lo = lo ^ __funnelshift_r(lo, hi, 12);
+        hi = hi ^ __umulhi(hi, args.p2[0]);                                // hi >> 12 on the FMA pipe
+    } else if constexpr (XS & 1) {
+        const uint64_t w = static_cast<uint64_t>(hi) * args.p2[0];         // {hi << 20, hi >> 12}
+        lo = lo ^ (lo >> 12) ^ static_cast<uint32_t>(w);
+        hi = hi ^ static_cast<uint32_t>(w >> 32);
+    } else {
+        lo = lo ^ __funnelshift_r(lo, hi, 12);
+        hi = hi ^ (hi >> 12);
+    }
+    // x ^= x << 25
+    if constexpr (XS & 2) {
+        const uint64_t w = static_cast<uint64_t>(lo) * args.p2[1];         // {lo << 25, lo >> 7}
+        hi = hi ^ (hi << 25) ^ static_cast<uint32_t>(w >> 32);
+        lo = lo ^ static_cast<uint32_t>(w);
+    } else {
+        hi = hi ^ __funnelshift_l(lo, hi, 25);
+        lo = lo ^ (lo << 25);
+    }
+    // x ^= x >> 27
+    if constexpr (XS & 8) {
+        lo = lo ^ __funnelshift_r(lo, hi, 27);
+        hi = hi ^ __umulhi(hi, args.p2[2]);                                // hi >> 27 on the FMA pipe
+    } else if constexpr (XS & 4) {
+        const uint64_t w = static_cast<uint64_t>(hi) * args.p2[2];         // {hi << 5, hi >> 27}
+        lo = lo ^ (lo >> 27) ^ static_cast<uint32_t>(w);
+        hi = hi ^ static_cast<uint32_t>(w >> 32);
+    } else {
+        lo = lo ^ __funnelshift_r(lo, hi, 27);
+        hi = hi ^ (hi >> 27);
+    }
+}
+
+// One SCS-1 round (R1-R9) for this thread.
+//   P        words per pick (1, 4, 8)
+//   SMEM     region in shared memory (else read from global)
+//   STRADDLE the region's chunk addresses may differ in their high 32 bits
+//            (else hi32(dp) == hi32(base) for every chunk, host-checked)
+//   XS       xorshift lowering (see xorshift_split)
+template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0>
+__device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
+                                           uint64_t base, uint32_t nc_mask, uint32_t src_lane,
+                                           const KernelArgs& args) {
     // R1
-    x = xorshift(x);
-    const uint64_t y = x * kXsMult;
+    xorshift_split<XS>(xlo, xhi, args);
+    const uint64_t y = ((static_cast<uint64_t>(xhi) << 32) | xlo) * kXsMult;
     // R2, R3
     const uint32_t C = a[kAccum - 1];
     const uint32_t i = (static_cast<uint32_t>(y >> 32) ^ C) & nc_mask;
-    // R5: data pointer of the chunk (also the global load address)
-    const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);
-    // R4
+    // R4, R5, R6 (first part)
     Pick<P> d;
-    if constexpr (SMEM) d = load_shared<P>(words + static_cast<size_t>(i) * P);
-    else d = load_global<P>(reinterpret_cast<const uint32_t*>(dp));
-    // R6
-    uint32_t t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(dp)) ^ static_cast<uint32_t>(dp >> 32);
+    uint32_t t;
+    if constexpr (SMEM && !STRADDLE && ADDR == 1) {
+        // shared-window address of the chunk on the FMA pipe; lo32(dp) = addr + (lo32(base) - smem)
+        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
+        d = load_shared_addr<P>(addr);
+        const uint32_t base_minus_smem = static_cast<uint32_t>(base) - smem_u32(smem_words);   // loop-invariant
+        t = ((static_cast<uint32_t>(y) ^ r) + addr + base_minus_smem) ^ static_cast<uint32_t>(base >> 32);
+    } else if constexpr (SMEM && !STRADDLE) {
+        const uint32_t v = i * (4u * P);                         // byte offset of the chunk
+        d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
+        t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(base) + v) ^ static_cast<uint32_t>(base >> 32);
+    } else {
+        const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);   // R5 (= the global load address)
+        if constexpr (SMEM) d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
+        else d = load_global<P, LD>(reinterpret_cast<const uint32_t*>(dp));
+        t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(dp)) ^ static_cast<uint32_t>(dp >> 32);
+    }
+    // R6 (data)
 #pragma unroll
     for (int q = 0; q < P; ++q) t = rotl(t, 5) + d.w[q];
     // R7
@@ -171,9 +274,8 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint64_t& x, u
     a[kAccum - 1] ^= __shfl_sync(0xFFFFFFFFu, t, src_lane);
 }
 
-template <int P, bool SMEM, int UNROLL>
+template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0>
 __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs args) {
-    extern __shared__ __align__(128) uint32_t smem_words[];
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint64_t t_start_ns;
@@ -186,7 +288,6 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
     }
 
     // a2: stage the region into shared memory (SMEM placement).
-    const uint32_t* words = args.region;
     if constexpr (SMEM) {
         const uint32_t bytes = args.region_bytes;
         if ((bytes & 15u) == 0) {
@@ -206,7 +307,6 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
             for (uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x) smem_words[k] = args.region[k];
             __syncthreads();
         }
-        words = smem_words;
     }
 
     // a1: I1-I3
@@ -221,6 +321,7 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
         x = xorshift(x);
         a[j] = static_cast<uint32_t>((x * kXsMult) >> 32);
     }
+    uint32_t xlo = static_cast<uint32_t>(x), xhi = static_cast<uint32_t>(x >> 32);
 
     const uint64_t base = reinterpret_cast<uint64_t>(args.region);
     const uint32_t nc_mask = args.nc_mask;
@@ -232,15 +333,15 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
     for (; r < main_end; r += UNROLL) {
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
-            scs1_round<P, SMEM>(a, x, r + u, words, base, nc_mask, src_lane, args);
+            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r + u, base, nc_mask, src_lane, args);
     }
-    for (; r < rounds; ++r) scs1_round<P, SMEM>(a, x, r, words, base, nc_mask, src_lane, args);
+    for (; r < rounds; ++r) scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r, base, nc_mask, src_lane, args);
 
     // a11: F1-F2
     uint32_t e = 0, o = 0;
 #pragma unroll
     for (int j = 0; j < kAccum; j += 2) { e ^= a[j]; o ^= a[j + 1]; }
-    uint64_t f = ((static_cast<uint64_t>(o) << 32) | e) ^ x;
+    uint64_t f = ((static_cast<uint64_t>(o) << 32) | e) ^ ((static_cast<uint64_t>(xhi) << 32) | xlo);
 
     // a12: warp -> block -> grid
 #pragma unroll
@@ -269,6 +370,15 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
                       static_cast<unsigned long long>(t_end_ns));
         }
     }
+}
+
+// Host-side helper: fill the constant-bank tables of KernelArgs.
+inline void fill_tables(KernelArgs& args, uint32_t P) {
+    args.four_p = 4u * P;
+    for (int j = 0; j < kAccum; ++j) args.mul[j] = mul_of(j);
+    args.p2[0] = 1u << 20;
+    args.p2[1] = 1u << 25;
+    args.p2[2] = 1u << 5;
 }
 
 }  // namespace sage
