@@ -54,16 +54,35 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def load_traffic(workload):
-    """dram bytes per launch from the committed ncu --set full summary, or None."""
+def load_traffic(workload, thread_rounds):
+    """DRAM bytes (read + write) per launch from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), or None.  Entries give bytes per
+    launch, or bytes per thread-round (scaled to this launch's n*R)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
             ent = json.load(f).get(workload)
         if isinstance(ent, dict):
+            if "dram_bytes_per_thread_round" in ent:
+                return ent["dram_bytes_per_thread_round"] * thread_rounds
             return ent.get("dram_bytes_per_launch")
         return ent
     return None
+
+
+def random_gather_ceiling(region_bytes):
+    """L0 probe (bench/microbench.cu): dependent random 4-B reads, one per
+    32-B sector, full occupancy, over a buffer of the same size -- the measured
+    ceiling for the pick pattern without any checksum arithmetic."""
+    exe = os.path.join(ROOT, "bench", "microbench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "gather", str(max(1, region_bytes >> 20))], capture_output=True, text=True,
+                             timeout=120).stdout
+        return json.loads(out.strip().splitlines()[-1])["picks_per_s"]
+    except (subprocess.SubprocessError, ValueError, IndexError, KeyError):
+        return None
 
 
 class ClockSampler:
@@ -175,16 +194,25 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2209_03125_b200 import build, sage
-    from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces
+    from paper_2209_03125_b200 import build, replicas, sage
+    from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region
 
     ws, rank, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
+    ndev = torch.cuda.device_count()
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = None
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # plumbing only (barrier, max-over-ranks, result gather); nccl when every
+        # rank owns a GPU, gloo when ranks share one (single-GPU test boxes)
+        backend = "nccl" if ndev >= ws else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     if rank == 0:
         build.build()
     if ws > 1:
@@ -202,6 +230,7 @@ def run_ours(args):
         g = torch.Generator(device=dev)
         g.manual_seed(0x5EED0001)
         region = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
+    gather_ceiling = random_gather_ceiling(nbytes) if (rank == 0 and nbytes > (1 << 20)) else None
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     blocks, threads = (1, 32) if args.config == "c1" else (0, 0)
@@ -209,7 +238,7 @@ def run_ours(args):
     info = ctx.query()
     n = info.blocks * info.threads
     placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
-    my_nonces = nonces(args.warmup + args.steps + 64, master_seed=0x220903125 + rank)
+    my_nonces = replicas.replica_nonces(rank, args.warmup + args.steps + 64)
     total = args.warmup + args.steps
     raw = torch.zeros(total, 4, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -242,16 +271,14 @@ def run_ours(args):
     launches = ctx.launches - launches0
     kern_s = [ev[k][0].elapsed_time(ev[k][1]) / 1e3 for k in range(args.warmup, total)]
     # the bracket, max over ranks
-    t_bracket = torch.tensor([t_wall], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t_bracket, op=dist.ReduceOp.MAX)
-    t_bracket = float(t_bracket.item())
+    pdev = dev if backend != "gloo" else None
+    t_bracket = replicas.max_over_ranks(t_wall, pdev)
     raws = raw.cpu().tolist()
     dec = [sage.decode_raw(r) for r in raws[args.warmup:]]
 
     # e2e through the public C API with HOST buffers (pinned): H2D of the
     # region + kernel + D2H of the 32-byte result, every step.
-    host_region = torch.from_numpy(region_np).pin_memory() if region_np is not None else None
+    host_region = (torch.from_numpy(region_np) if region_np is not None else region.cpu()).pin_memory()
     e2e = None
     if host_region is not None:
         ctx_h = sage.Context(device=local, blocks=blocks, threads=threads, pick_words=P, stream=stream)
@@ -265,10 +292,8 @@ def run_ours(args):
         for k in range(args.steps):
             r = ctx_h.attest_host(my_nonces[args.warmup + k], host_region, R)
             e2e_ns.append(r.elapsed_ns)
-        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * n * R * args.steps / float(t_e2e.item()), "unit": UNIT,
+        t_e2e = replicas.max_over_ranks(time.perf_counter() - t0, pdev)
+        e2e = {"value": ws * n * R * args.steps / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32,
                "api": "sage_attest_host (pinned host region)"}
         ctx_h.close()
@@ -285,13 +310,11 @@ def run_ours(args):
     parts = [int(v) & (2**64 - 1) for v in pw.cpu().tolist()]
 
     # gather per-replica results to rank 0 (the only cross-GPU step, 8(e))
-    mine = {"rank": rank, "checksum": "0x%016x" % dec[-1].checksum, "cycles": dec[-1].cycles,
-            "device_ns": dec[-1].device_ns, "kernel_ms_mean": 1e3 * statistics.mean(kern_s)}
-    if ws > 1:
-        allr = [None] * ws
-        dist.all_gather_object(allr, mine)
-    else:
-        allr = [mine]
+    mine = {"rank": rank, "device": local, "nonce": "0x%016x" % my_nonces[total - 1],
+            "checksum": "0x%016x" % dec[-1].checksum, "cycles": dec[-1].cycles,
+            "device_ns": dec[-1].device_ns, "kernel_ms_mean": 1e3 * statistics.mean(kern_s),
+            "sampled_parity_sum_ok": (sum(parts) & (2**64 - 1)) == dbg.checksum}
+    allr = replicas.gather_results(mine)
 
     if rank == 0:
         peaks, peak_src = load_peaks()
@@ -305,7 +328,8 @@ def run_ours(args):
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": {"workload": args.config, "desc": desc, "region_bytes": nbytes, "P": P, "rounds": R,
                            "blocks": info.blocks, "threads": info.threads, "threads_total": n,
-                           "placement": placement, "parallelism": "replica x%d" % ws,
+                           "placement": placement, "parallelism": "independent replica per GPU x%d" % ws,
+                           "plumbing": backend or "none",
                            "l2": "256 MiB buffer written between timed steps (flush)"},
                 "checksummed_gbps": value * 4 * P / 1e9,
                 "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(kern_s), "max": 1e3 * max(kern_s)},
@@ -315,15 +339,18 @@ def run_ours(args):
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
         if placement == "global" and nbytes > (1 << 20):
             achieved = n * R * 32.0 / mean_k / 1e9       # DRAM sectors touched (one 32-B sector per pick)
+            ceil = gather_ceiling
             line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic(args.config),
+                                "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic(args.config, n * R),
                                 "peak_source": peak_src + " hbm_gbs (copy)",
-                                "achieved_def": "one 32-B DRAM sector per pick x n x R / kernel time"}
+                                "achieved_def": "one 32-B sector per pick x n x R / kernel time",
+                                "random_gather_ceiling_picks_per_s": ceil,
+                                "frac_of_random_gather_ceiling": (n * R / mean_k / ceil) if ceil else None}
         else:
             peak_ops = sms * 4 * 32 * f_clk / 1e12
             achieved = n * R * ops / mean_k / 1e12
             line["roofline"] = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
-                                "frac": achieved / peak_ops, "traffic": load_traffic(args.config),
+                                "frac": achieved / peak_ops, "traffic": load_traffic(args.config, n * R),
                                 "peak_source": "%d SMs x 4 SMSP x 32 lanes x 1 issue/clk x %s sm_max_mhz %.0f "
                                                "(DESIGN.md 7)" % (sms, peak_src, f_clk / 1e6),
                                 "ops_per_thread_round": ops}

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #define CK(x)                                                                  \
@@ -99,7 +100,62 @@ __global__ void __launch_bounds__(1024, 2) p_hbm_gather(Args a, const uint32_t* 
     if (threadIdx.x == 0) atomicMax(a.cycles, (unsigned long long)(t1 - t0));
 }
 
-int main() {
+// MLP-k dependent random gathers: k independent chains per thread, one 4-B load
+// per 32-B sector, over `mask+1` sectors.  Tells whether random HBM reads are
+// latency-bound (rate grows with k) or transaction-bound (flat in k).
+template <int K>
+__global__ void __launch_bounds__(1024, 2) p_hbm_gather_mlp(Args a, const uint32_t* __restrict__ buf, uint32_t mask) {
+    uint32_t x[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) x[k] = (blockIdx.x * blockDim.x + threadIdx.x) * 0x9E3779B9u + a.c3 + 77u * k;
+    for (uint32_t it = 0; it < a.iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            x[k] = x[k] * 1664525u + 1013904223u;
+            uint32_t w;
+            asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w) : "l"(buf + ((x[k] >> 3) & mask) * 8u));
+            x[k] ^= w;
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s ^= x[k];
+    if (s == 0x12345679u) a.sink[0] = s;
+}
+
+int gather_only(size_t mb) {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    Args a{};
+    a.c3 = 7;
+    CK(cudaMalloc(&a.sink, 4));
+    size_t bytes = mb << 20;
+    uint32_t* buf = nullptr;
+    CK(cudaMalloc(&buf, bytes));
+    CK(cudaMemset(buf, 1, bytes));
+    uint32_t mask = uint32_t(bytes / 32 - 1);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    a.iters = 2048;
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaEventRecord(e0));
+        p_hbm_gather_mlp<1><<<2 * sms, 1024>>>(a, buf, mask);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) best = ms;
+    }
+    double picks = double(2 * sms) * 1024 * a.iters;
+    printf("{\"probe\": \"hbm_gather_mlp\", \"mib\": %zu, \"mlp\": 1, \"picks_per_s\": %.4e, \"ms\": %.3f}\n",
+           mb, picks / (best * 1e-3), best);
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc > 2 && strcmp(argv[1], "gather") == 0) return gather_only(strtoull(argv[2], nullptr, 10));
     int dev = 0, sms = 0, clk = 0;
     CK(cudaSetDevice(dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -173,6 +229,30 @@ int main() {
         double picks = double(blocks) * threads * a.iters;
         printf("{\"probe\": \"hbm_dependent_sector_gather\", \"gib\": %zu, \"picks_per_s\": %.4e, "
                "\"sector_gbps\": %.1f, \"ms\": %.3f}\n", gib, picks / (ms * 1e-3), picks * 32 / (ms * 1e-3) / 1e9, ms);
+        CK(cudaFree(buf));
+    }
+    for (size_t mb : {256, 2048}) {
+        size_t bytes = mb << 20;
+        uint32_t* buf = nullptr;
+        CK(cudaMalloc(&buf, bytes));
+        CK(cudaMemset(buf, 1, bytes));
+        uint32_t mask = uint32_t(bytes / 32 - 1);
+        void (*fns[])(Args, const uint32_t*, uint32_t) = {p_hbm_gather_mlp<1>, p_hbm_gather_mlp<2>, p_hbm_gather_mlp<4>};
+        int ks[] = {1, 2, 4};
+        for (int f = 0; f < 3; ++f) {
+            a.iters = 2048 / ks[f];
+            float ms = 0;
+            for (int rep = 0; rep < 2; ++rep) {
+                CK(cudaEventRecord(e0));
+                fns[f]<<<blocks, threads>>>(a, buf, mask);
+                CK(cudaEventRecord(e1));
+                CK(cudaEventSynchronize(e1));
+            }
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            double picks = double(blocks) * threads * a.iters * ks[f];
+            printf("{\"probe\": \"hbm_gather_mlp\", \"mib\": %zu, \"mlp\": %d, \"picks_per_s\": %.4e, \"ms\": %.3f}\n",
+                   mb, ks[f], picks / (ms * 1e-3), ms);
+        }
         CK(cudaFree(buf));
     }
     return 0;

@@ -94,41 +94,45 @@ __device__ __forceinline__ uint64_t globaltimer() {
 template <int P> struct Pick { uint32_t w[P]; };
 
 // Read-only global loads of one P-word chunk.  LD selects the cache policy:
-//   0: ld.global.nc                      (L1-allocating; small, L1-resident regions)
-//   1: ld.global.nc.L1::no_allocate      (sector-granular L2 requests; L2/HBM regions)
-//   2: ld.global.cg                      (cache at L2 only)
+//   0: ld.global.nc                          (L1-allocating; small, L1-resident regions)
+//   1: ld.global.nc.L1::no_allocate          (no L1 allocation)
+//   2: ld.global.cg                          (cache at L2 only)
+//   3: ld.global.nc.L2::64B                  (64-B L2 fetch hint)
+//   4: ld.global.nc.L1::no_allocate.L2::cache_hint with an evict_first policy
 template <int P, int LD>
-__device__ __forceinline__ Pick<P> load_global(const uint32_t* p) {
+__device__ __forceinline__ Pick<P> load_global(const uint32_t* p, uint64_t policy) {
     Pick<P> d;
+    uint32_t* w = d.w;
     if constexpr (P == 1) {
-        if constexpr (LD == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
-        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
-        else asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(d.w[0]) : "l"(p));
+        if constexpr (LD == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+        else if constexpr (LD == 2) asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+        else if constexpr (LD == 3) asm volatile("ld.global.nc.L2::64B.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+        else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(w[0]) : "l"(p), "l"(policy));
     } else if constexpr (P == 4) {
-        if constexpr (LD == 0)
-            asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
-        else if constexpr (LD == 1)
-            asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
-        else
-            asm volatile("ld.global.cg.v4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]) : "l"(p));
+#define O4 "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+        if constexpr (LD == 0) asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
+        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
+        else if constexpr (LD == 2) asm volatile("ld.global.cg.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
+        else if constexpr (LD == 3) asm volatile("ld.global.nc.L2::64B.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
+        else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;" : O4 : "l"(p), "l"(policy));
+#undef O4
     } else {
-        if constexpr (LD == 0)
-            asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
-                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
-        else if constexpr (LD == 1)
-            asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
-                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
-        else
-            asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
-                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7]) : "l"(p));
+#define O8 "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+        if constexpr (LD == 0) asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
+        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
+        else if constexpr (LD == 2) asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
+        else if constexpr (LD == 3) asm volatile("ld.global.nc.L2::64B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
+        else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;" : O8 : "l"(p), "l"(policy));
+#undef O8
     }
     return d;
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 template <int P>
@@ -233,7 +237,7 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0>
 __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
-                                           const KernelArgs& args) {
+                                           const KernelArgs& args, uint64_t policy = 0) {
     // R1
     xorshift_split<XS>(xlo, xhi, args);
     const uint64_t y = ((static_cast<uint64_t>(xhi) << 32) | xlo) * kXsMult;
@@ -256,7 +260,7 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
     } else {
         const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);   // R5 (= the global load address)
         if constexpr (SMEM) d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
-        else d = load_global<P, LD>(reinterpret_cast<const uint32_t*>(dp));
+        else d = load_global<P, LD>(reinterpret_cast<const uint32_t*>(dp), policy);
         t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(dp)) ^ static_cast<uint32_t>(dp >> 32);
     }
     // R6 (data)
@@ -326,6 +330,8 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
     const uint64_t base = reinterpret_cast<uint64_t>(args.region);
     const uint32_t nc_mask = args.nc_mask;
     const uint32_t rounds = args.rounds;
+    uint64_t policy = 0;
+    if constexpr (LD == 4) policy = evict_first_policy();
 
     // a10: round loop, UNROLL rounds per trip + remainder
     uint32_t r = 0;
@@ -333,9 +339,9 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
     for (; r < main_end; r += UNROLL) {
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
-            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r + u, base, nc_mask, src_lane, args);
+            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r + u, base, nc_mask, src_lane, args, policy);
     }
-    for (; r < rounds; ++r) scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r, base, nc_mask, src_lane, args);
+    for (; r < rounds; ++r) scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r, base, nc_mask, src_lane, args, policy);
 
     // a11: F1-F2
     uint32_t e = 0, o = 0;
