@@ -1,0 +1,119 @@
+// adversary.cu -- Table 1 Exp 1 vs Exp 2 on B200.
+//
+// The paper measures the honest checksum 100 times (T_avg, sigma), sets the
+// detection threshold at T_avg + 2.5 sigma, then inserts ONE extra
+// instruction into the checksum loop and shows that even its fastest run
+// T_min exceeds the threshold (Table 1).  Here the
+// honest kernel is the product's c2a kernel (full occupancy, 8 KiB SMEM
+// region, P=1) and each adversary is the same kernel with EXTRA
+// result-neutral dependent ALU instructions injected once every UNROLL
+// rounds (so it still returns the correct checksum).  Timing is the
+// verifier's: host CLOCK_MONOTONIC from before the launch to the result on
+// the host (as in sage_attest).  One JSON line per kernel, then a summary.
+//
+//   ./adversary [rounds=100000] [runs=100]
+#include <cuda_runtime.h>
+#include <time.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "sage_kernel.cuh"
+
+#define CK(x)                                                                  \
+    do {                                                                       \
+        cudaError_t e = (x);                                                   \
+        if (e != cudaSuccess) {                                                \
+            fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e));            \
+            exit(1);                                                           \
+        }                                                                      \
+    } while (0)
+
+using Fn = void (*)(const sage::KernelArgs);
+struct K { const char* name; Fn fn; int extra; int every; };
+
+// <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA>
+static K kernels[] = {
+    {"honest unroll1", sage::sage_checksum_kernel<1, true, false, 0, 1, 1, 0, 0>, 0, 1},
+    {"honest unroll8", sage::sage_checksum_kernel<1, true, false, 0, 8, 1, 0, 0>, 0, 8},
+    {"+1 instr / round", sage::sage_checksum_kernel<1, true, false, 0, 1, 1, 0, 1>, 1, 1},
+    {"+1 instr / 8 rounds", sage::sage_checksum_kernel<1, true, false, 0, 8, 1, 0, 1>, 1, 8},
+};
+
+static uint64_t now_ns() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return uint64_t(ts.tv_sec) * 1000000000ull + uint64_t(ts.tv_nsec);
+}
+
+int main(int argc, char** argv) {
+    const uint32_t rounds = argc > 1 ? atoi(argv[1]) : 100000;
+    const int runs = argc > 2 ? atoi(argv[2]) : 100;
+    const size_t bytes = 8192;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int blocks = 2 * sms, threads = 1024;
+    std::vector<uint8_t> h(bytes);
+    srand(11);
+    for (auto& b : h) b = rand() & 0xFF;
+    uint8_t* d = nullptr;
+    CK(cudaMalloc(&d, bytes));
+    CK(cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice));
+    uint64_t *raw = nullptr, *hraw = nullptr;
+    CK(cudaMalloc(&raw, 32));
+    CK(cudaMallocHost(&hraw, 32));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct Stat { double avg, sd, mn, mx; uint64_t cs; };
+    std::vector<Stat> st;
+    for (auto& k : kernels) {
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)bytes));
+        sage::KernelArgs a{};
+        a.region = reinterpret_cast<const uint32_t*>(d);
+        a.nonce = 0xA77E57;
+        a.nc_mask = uint32_t(bytes / 4 - 1);
+        a.rounds = rounds;
+        a.region_bytes = uint32_t(bytes);
+        a.raw = raw;
+        sage::fill_tables(a, 1);
+        std::vector<double> t;
+        uint64_t cs = 0;
+        for (int i = -3; i < runs; ++i) {      // 3 warm-up runs
+            const uint64_t t0 = now_ns();
+            CK(cudaMemsetAsync(raw, 0, 32, s));
+            k.fn<<<blocks, threads, bytes, s>>>(a);
+            CK(cudaMemcpyAsync(hraw, raw, 32, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const uint64_t t1 = now_ns();
+            if (i >= 0) t.push_back((t1 - t0) * 1e-9);
+            cs = hraw[0];
+        }
+        double m = 0, v = 0;
+        for (double x : t) m += x;
+        m /= t.size();
+        for (double x : t) v += (x - m) * (x - m);
+        v /= t.size();
+        Stat q{m, std::sqrt(v), *std::min_element(t.begin(), t.end()), *std::max_element(t.begin(), t.end()), cs};
+        st.push_back(q);
+        printf("{\"kernel\": \"%s\", \"extra_instr\": %d, \"every_rounds\": %d, \"runs\": %d, \"t_avg_s\": %.6f, "
+               "\"sigma_s\": %.6f, \"t_min_s\": %.6f, \"t_max_s\": %.6f, \"threshold_s\": %.6f, \"checksum\": \"0x%016llx\"}\n",
+               k.name, k.extra, k.every, runs, q.avg, q.sd, q.mn, q.mx, q.avg + 2.5 * q.sd, (unsigned long long)cs);
+        fflush(stdout);
+    }
+    // verdicts: adversary vs the honest kernel with the same unroll
+    const int pairs[][2] = {{0, 2}, {1, 3}};
+    for (auto& p : pairs) {
+        const Stat& hs = st[p[0]];
+        const Stat& as = st[p[1]];
+        const double thr = hs.avg + 2.5 * hs.sd;
+        printf("{\"summary\": \"%s vs %s\", \"honest_t_avg_s\": %.6f, \"honest_sigma_s\": %.6f, \"threshold_s\": %.6f, "
+               "\"adversary_t_min_s\": %.6f, \"slowdown\": %.5f, \"detected\": %s, \"same_checksum\": %s}\n",
+               kernels[p[1]].name, kernels[p[0]].name, hs.avg, hs.sd, thr, as.mn, as.avg / hs.avg - 1.0,
+               as.mn > thr ? "true" : "false", hs.cs == as.cs ? "true" : "false");
+    }
+    return 0;
+}

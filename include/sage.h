@@ -100,13 +100,21 @@ int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
 
 /* Asynchronous form: validates, then enqueues the checksum kernel on the
  * context's stream and returns.  raw_out is a DEVICE buffer of 4 u64 that the
- * kernel accumulates into and that the caller zeroes before the launch
- * (sage_attest_async zeroes it on the same stream unless it is NULL):
+ * kernel accumulates into and that the CALLER must zero (on the same stream)
+ * before the launch:
  *   raw_out[0] checksum, [1] max CTA cycles, [2] ~(first CTA start ns),
  *   [3] last CTA end ns.  per_warp_out may be NULL.  Decode with
  *   sage_decode_raw.  Safe to capture in a CUDA graph. */
 int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
                       uint64_t rounds, uint64_t* raw_out, uint64_t* per_warp_out);
+
+/* Inclusion experiment: as sage_attest with GLOBAL placement,
+ * and also counts how often each chunk is read.  counts_out: DEVICE buffer of
+ * Nc = region_bytes / (4 * P) u32, zeroed by the call.  The checksum is the
+ * same as sage_attest's for the same inputs; the timing is not representative
+ * (one global atomic per pick). */
+int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
+                         uint64_t rounds, uint32_t* counts_out, sage_result* out);
 
 /* Decode a raw 4 x u64 result (host copy) into checksum / cycles / device_ns. */
 int sage_decode_raw(const uint64_t raw[4], sage_result* out);

@@ -56,6 +56,16 @@ KernelFn kernel_for_p(bool smem, bool straddle) {
     return sage::sage_checksum_kernel<P, false, true, 0, 1, 0, 0>;
 }
 
+// Inclusion-experiment variant (counts reads per chunk); GLOBAL placement.
+KernelFn counting_kernel_for(uint32_t P) {
+    switch (P) {
+        case 1: return sage::sage_checksum_kernel<1, false, true, 0, 1, 0, 0, 0, true>;
+        case 4: return sage::sage_checksum_kernel<4, false, true, 0, 1, 0, 0, 0, true>;
+        case 8: return sage::sage_checksum_kernel<8, false, true, 0, 1, 0, 0, 0, true>;
+        default: return nullptr;
+    }
+}
+
 KernelFn kernel_for(uint32_t P, bool smem, bool straddle) {
     switch (P) {
         case 1: return kernel_for_p<1>(smem, straddle);
@@ -114,14 +124,14 @@ uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
 }
 
 int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
-           uint64_t* per_warp, uint32_t* placement_used) {
-    const uint32_t placement = choose_placement(c, bytes);
+           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr) {
+    const uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
     if (placement == SAGE_SMEM && bytes > kSmemRegionMax)
         return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s", "64 KiB");
     const bool smem = placement == SAGE_SMEM;
     const uint64_t lo = reinterpret_cast<uint64_t>(region);
     const bool straddle = (lo >> 32) != ((lo + bytes - 1) >> 32);
-    KernelFn fn = kernel_for(c->pick_words, smem, straddle);
+    KernelFn fn = counts ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle);
     const size_t dyn = smem ? bytes : 0;
     if (smem) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
@@ -133,6 +143,7 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     args.region_bytes = static_cast<uint32_t>(smem ? bytes : 0);
     args.raw = raw;
     args.per_warp = per_warp;
+    args.counts = counts;
     sage::fill_tables(args, c->pick_words);
     fn<<<c->blocks, c->threads, dyn, c->stream>>>(args);
     CUDA_TRY(cudaGetLastError());
@@ -154,14 +165,14 @@ void fill_result(const sage_ctx* c, const uint64_t raw[4], uint64_t t0, uint64_t
 
 // attest synchronously over a device region already validated
 int attest_device(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds,
-                  uint64_t* per_warp, sage_result* out, const void* host_src) {
+                  uint64_t* per_warp, sage_result* out, const void* host_src, uint32_t* counts = nullptr) {
     int rc = set_device(c);
     if (rc) return rc;
     const uint64_t t0 = now_ns();
     if (host_src) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(region), host_src, bytes, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_raw, 0, 4 * sizeof(uint64_t), c->stream));
     uint32_t placement = 0;
-    rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement);
+    rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->h_raw, c->d_raw, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -251,6 +262,21 @@ int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     rc = set_device(ctx);
     if (rc) return rc;
     return launch(ctx, nonce, region, region_bytes, rounds, raw_out, per_warp_out, nullptr);
+}
+
+int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes, uint64_t rounds,
+                         uint32_t* counts_out, sage_result* out) {
+    int rc = validate(ctx, region, region_bytes, rounds);
+    if (rc) return rc;
+    if (counts_out == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    rc = set_device(ctx);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(counts_out, 0, region_bytes / (4ull * ctx->pick_words) * sizeof(uint32_t), ctx->stream));
+    sage_result tmp;
+    rc = attest_device(ctx, nonce, region, region_bytes, rounds, nullptr, &tmp, nullptr, counts_out);
+    if (rc) return rc;
+    *out = tmp;
+    return SAGE_OK;
 }
 
 int sage_decode_raw(const uint64_t raw[4], sage_result* out) {

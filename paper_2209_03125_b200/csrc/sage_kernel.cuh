@@ -181,6 +181,8 @@ struct KernelArgs {
     // (constant bank, so ptxas cannot turn them back into ALU shifts).
     uint32_t p2[3];
     uint32_t four_p;          // 4*P as a runtime value (forces IMAD for the chunk offset)
+    uint32_t zero;            // 0; operand of the injected instructions of EXTRA > 0 (timing adversary)
+    uint32_t* counts;         // COUNT variant only: per-chunk read counters (inclusion experiment)
 };
 
 // The region staged in shared memory (SMEM placement): namespace-scope so the
@@ -234,16 +236,24 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 //   STRADDLE the region's chunk addresses may differ in their high 32 bits
 //            (else hi32(dp) == hi32(base) for every chunk, host-checked)
 //   XS       xorshift lowering (see xorshift_split)
-template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0>
+//   EXTRA    number of result-neutral instructions injected (when `inject`) into
+//            the round (0 in the product; > 0 only for the timing-adversary
+//            experiment, the B200 analogue of Table 1 Exp 2's
+//            "adversarial NOP"; the kernel injects them in the first
+//            round of every UNROLL-round trip)
+//   COUNT    also count reads per chunk into args.counts (the memory-region
+//            inclusion experiment); not in the timed path
+template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false>
 __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
-                                           const KernelArgs& args, uint64_t policy = 0) {
+                                           const KernelArgs& args, uint64_t policy = 0, bool inject = false) {
     // R1
     xorshift_split<XS>(xlo, xhi, args);
     const uint64_t y = ((static_cast<uint64_t>(xhi) << 32) | xlo) * kXsMult;
     // R2, R3
     const uint32_t C = a[kAccum - 1];
     const uint32_t i = (static_cast<uint32_t>(y >> 32) ^ C) & nc_mask;
+    if constexpr (COUNT) atomicAdd(&args.counts[i], 1u);
     // R4, R5, R6 (first part)
     Pick<P> d;
     uint32_t t;
@@ -272,13 +282,19 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
         a[j] = a[j] * args.mul[j] + t;
         t = a[j] + rotl(t, rot_of(j));
     }
+    // injected adversary work: dependent ALU ops that leave t unchanged (t ^ 0)
+    if (inject) {
+#pragma unroll
+        for (int e = 0; e < EXTRA; ++e) t ^= args.zero;
+    }
     // R8
     t = t + (t >> (C & 31u));
     // R9
     a[kAccum - 1] ^= __shfl_sync(0xFFFFFFFFu, t, src_lane);
 }
 
-template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0>
+template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
+          bool COUNT = false>
 __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
@@ -339,9 +355,11 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
     for (; r < main_end; r += UNROLL) {
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
-            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r + u, base, nc_mask, src_lane, args, policy);
+            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a, xlo, xhi, r + u, base, nc_mask, src_lane, args, policy,
+                                                                  u == 0);
     }
-    for (; r < rounds; ++r) scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD>(a, xlo, xhi, r, base, nc_mask, src_lane, args, policy);
+    for (; r < rounds; ++r)
+        scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a, xlo, xhi, r, base, nc_mask, src_lane, args, policy, true);
 
     // a11: F1-F2
     uint32_t e = 0, o = 0;
@@ -381,6 +399,7 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
 // Host-side helper: fill the constant-bank tables of KernelArgs.
 inline void fill_tables(KernelArgs& args, uint32_t P) {
     args.four_p = 4u * P;
+    args.zero = 0;
     for (int j = 0; j < kAccum; ++j) args.mul[j] = mul_of(j);
     args.p2[0] = 1u << 20;
     args.p2[1] = 1u << 25;

@@ -21,7 +21,7 @@ PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto"}
 
 # every symbol include/sage.h declares
 EXPORTS = ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
-           "sage_attest_host", "sage_host_region_va", "sage_placement_for", "sage_query", "sage_launch_count",
+           "sage_attest_host", "sage_attest_coverage", "sage_host_region_va", "sage_placement_for", "sage_query", "sage_launch_count",
            "sage_stream", "sage_checksum_destroy", "sage_strerror", "sage_last_error")
 
 
@@ -72,6 +72,7 @@ def load(path=LIB):
     L.sage_attest_debug.argtypes = [p, u64, p, sz, u64, p, ctypes.POINTER(sage_result)]
     L.sage_attest_async.argtypes = [p, u64, p, sz, u64, p, p]
     L.sage_decode_raw.argtypes = [p, ctypes.POINTER(sage_result)]
+    L.sage_attest_coverage.argtypes = [p, u64, p, sz, u64, p, ctypes.POINTER(sage_result)]
     L.sage_attest_host.argtypes = [p, u64, p, sz, u64, ctypes.POINTER(sage_result)]
     L.sage_host_region_va.argtypes = [p, sz, ctypes.POINTER(u64)]
     L.sage_placement_for.argtypes = [p, sz, ctypes.POINTER(ctypes.c_uint32)]
@@ -87,7 +88,8 @@ def load(path=LIB):
     L.sage_last_error.argtypes = []
     L.sage_last_error.restype = ctypes.c_char_p
     for name in ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
-                 "sage_attest_host", "sage_host_region_va", "sage_placement_for", "sage_query"):
+                 "sage_attest_coverage",
+                 "sage_attest_host", "sage_attest_coverage", "sage_host_region_va", "sage_placement_for", "sage_query"):
         getattr(L, name).restype = i
     _lib = L
     return L
@@ -163,6 +165,13 @@ def attest_async(ctx, nonce, region, rounds, raw_out, per_warp_out=None, nbytes=
                                     _ptr(per_warp_out)))
 
 
+def attest_coverage(ctx, nonce, region, rounds, counts_out, nbytes=None):
+    out = sage_result()
+    _check(load().sage_attest_coverage(ctx, nonce, _ptr(region), _nbytes(region, nbytes), rounds, _ptr(counts_out),
+                                       ctypes.byref(out)))
+    return out
+
+
 def decode_raw(raw4):
     """raw4: host sequence of 4 u64 (e.g. raw_out.cpu())."""
     arr = (ctypes.c_uint64 * 4)(*[int(v) & (2**64 - 1) for v in raw4])
@@ -231,6 +240,9 @@ class Context:
 
     def attest_async(self, nonce, region, rounds, raw_out, per_warp_out=None, nbytes=None):
         return attest_async(self.ctx, nonce, region, rounds, raw_out, per_warp_out, nbytes)
+
+    def attest_coverage(self, nonce, region, rounds, counts_out, nbytes=None):
+        return attest_coverage(self.ctx, nonce, region, rounds, counts_out, nbytes)
 
     def attest_host(self, nonce, host_region, rounds, nbytes=None):
         return attest_host(self.ctx, nonce, host_region, rounds, nbytes)

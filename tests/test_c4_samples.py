@@ -1,0 +1,32 @@
+"""CPU check of the stored config-4 samples: the per-warp partials recorded by
+scripts/timing_distribution.py on the B200 (from the GPU kernel) are recomputed
+by the oracle on the same region bytes and device VA.  Skips when no capture
+is committed.  Only R <= 10^6 samples are recomputed (one warp at 10^6 rounds
+is ~1 s of oracle time)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01",
+                    "c4_timing.json")
+
+
+@pytest.mark.skipif(not os.path.exists(PATH), reason="no config-4 capture committed")
+def test_c4_sampled_warps_match_oracle():
+    with open(PATH) as f:
+        d = json.load(f)
+    region = np.frombuffer(bytes.fromhex(d["region_hex"]), dtype=np.uint8)
+    checked = 0
+    for ent in d["per_R"]:
+        assert ent["sum_of_partials_ok"] == ent["n_attest"]
+        if ent["rounds"] > 1_000_000:
+            continue
+        for s in ent["samples"][: (2 if ent["rounds"] >= 1_000_000 else 4)]:
+            want = oracle.warp_sum(s["nonce"], region, d["region_va"], ent["rounds"], s["warp"], d["P"])
+            assert want == s["warp_partial"], (ent["rounds"], s)
+            checked += 1
+    assert checked > 0

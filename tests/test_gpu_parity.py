@@ -66,11 +66,15 @@ def test_random_small_geometries(dev, seed):
         nonce = int(rng.integers(0, 2**64, dtype=np.uint64))
         region = make_region(nbytes, fill_seed=int(rng.integers(0, 2**31)))
         d, _keep = to_dev(region, dev, align_offset=32 * int(rng.integers(0, 8)))
+        pw = torch.zeros(blocks * threads // 32, dtype=torch.int64, device=dev)
         with sage.Context(blocks=blocks, threads=threads, pick_words=P, placement=placement) as ctx:
-            res = ctx.attest(nonce, d, rounds)
+            res = ctx.attest_debug(nonce, d, rounds, pw)
         want = oracle.attest(nonce, region, d.data_ptr(), rounds, blocks, threads, P)
         assert res.checksum == want, dict(P=P, nc=nc, placement=placement, blocks=blocks, threads=threads,
                                           rounds=rounds)
+        parts = [int(v) & M64 for v in pw.cpu().tolist()]
+        w = int(rng.integers(0, len(parts)))
+        assert parts[w] == oracle.warp_sum(nonce, region, d.data_ptr(), rounds, w, P)
 
 
 def test_tiny_regions_below_bulk_granule(dev):
@@ -151,7 +155,7 @@ def test_hbm_region_sampled(dev, P):
     g.manual_seed(P)
     d = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
     region = d.cpu().numpy()
-    R = 500
+    R = 10_000                                           # bench.py's c3 round count
     with sage.Context(pick_words=P) as ctx:
         info = ctx.query()
         n = info.blocks * info.threads
@@ -245,3 +249,50 @@ def test_argument_errors(dev):
         with pytest.raises(sage.SageError) as e:
             ctx.attest(0, region, 1, nbytes=1 << 20)
         assert e.value.code == sage.SAGE_EUNSUPPORTED
+
+
+def test_maximum_chunk_count(dev):
+    """Nc = 2^32 (the SCS-1 maximum): a 16 GiB P=1 region, mask 0xFFFFFFFF,
+    64-bit chunk offsets.  Zero-filled except one marker word per 64 MiB on both
+    sides (the host copy is a lazily-allocated numpy zeros array)."""
+    import numpy as np
+    nbytes = 1 << 34
+    try:
+        d = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    except RuntimeError:
+        pytest.skip("not enough device memory")
+    host = np.zeros(nbytes, dtype=np.uint8)
+    for k in range(0, nbytes, 64 << 20):
+        host[k:k + 4] = np.frombuffer((k // (64 << 20) + 1).to_bytes(4, "little"), dtype=np.uint8)
+        d[k:k + 4] = torch.from_numpy(host[k:k + 4].copy()).to(dev)
+    with sage.Context(blocks=2, threads=64) as ctx:
+        res = ctx.attest(0xBEEF, d, 300)
+        assert res.placement == sage.SAGE_GLOBAL
+    assert res.checksum == oracle.attest(0xBEEF, host, d.data_ptr(), 300, 2, 64, 1)
+    del d
+
+
+def test_multiple_waves(dev):
+    """More CTAs than fit at once (3 x SMs x 1024 threads): the result is the
+    same function of the linear thread index."""
+    region = make_region(4096, fill_seed=9)
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=1, threads=32) as c0:
+        sms = c0.query().sm_count
+    blocks = 3 * sms
+    pw = torch.zeros(blocks * 1024 // 32, dtype=torch.int64, device=dev)
+    with sage.Context(blocks=blocks, threads=1024) as ctx:
+        res = ctx.attest_debug(21, d, 40, pw)
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    assert sum(parts) & M64 == res.checksum
+    for w in (0, len(parts) // 2, len(parts) - 1):
+        assert parts[w] == oracle.warp_sum(21, region, d.data_ptr(), 40, w, 1)
+
+
+def test_p8_auto_placement_is_global(dev):
+    region = make_region(8192, prefix=kernel_code_prefix(8, False))
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=2, threads=96, pick_words=8) as ctx:
+        assert ctx.placement_for(8192) == sage.SAGE_GLOBAL
+        res = ctx.attest(0x88, d, 250)
+    assert res.checksum == oracle.attest(0x88, region, d.data_ptr(), 250, 2, 96, 8)
