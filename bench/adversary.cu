@@ -9,7 +9,8 @@
 // result-neutral dependent ALU instructions injected once every UNROLL
 // rounds (so it still returns the correct checksum).  Timing is the
 // verifier's: host CLOCK_MONOTONIC from before the launch to the result on
-// the host (as in sage_attest).  One JSON line per kernel, then a summary.
+// the host (as in sage_attest); the kernels are interleaved run by run.
+// One JSON line per kernel, then a summary per honest/adversary pair.
 //
 //   ./adversary [rounds=100000] [runs=100]
 #include <cuda_runtime.h>
@@ -67,12 +68,18 @@ int main(int argc, char** argv) {
     CK(cudaMallocHost(&hraw, 32));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct Stat { double avg, sd, mn, mx; uint64_t cs; };
+    struct Stat { double avg, sd, mn, mx, med, mad; uint64_t cs; std::vector<double> t; };
     std::vector<Stat> st;
-    for (auto& k : kernels) {
-        CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)bytes));
-        sage::KernelArgs a{};
+    // all kernels interleaved run by run, so drift (clocks, temperature) hits them alike
+    const int nk = sizeof(kernels) / sizeof(kernels[0]);
+    std::vector<sage::KernelArgs> args(nk);
+    std::vector<std::vector<double>> times(nk);
+    std::vector<uint64_t> sums(nk, 0);
+    for (int j = 0; j < nk; ++j) {
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernels[j].fn),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        sage::KernelArgs& a = args[j];
+        a = sage::KernelArgs{};
         a.region = reinterpret_cast<const uint32_t*>(d);
         a.nonce = 0xA77E57;
         a.nc_mask = uint32_t(bytes / 4 - 1);
@@ -80,28 +87,40 @@ int main(int argc, char** argv) {
         a.region_bytes = uint32_t(bytes);
         a.raw = raw;
         sage::fill_tables(a, 1);
-        std::vector<double> t;
-        uint64_t cs = 0;
-        for (int i = -3; i < runs; ++i) {      // 3 warm-up runs
+    }
+    for (int i = -3; i < runs; ++i) {           // 3 warm-up passes
+        for (int j = 0; j < nk; ++j) {
             const uint64_t t0 = now_ns();
             CK(cudaMemsetAsync(raw, 0, 32, s));
-            k.fn<<<blocks, threads, bytes, s>>>(a);
+            kernels[j].fn<<<blocks, threads, bytes, s>>>(args[j]);
             CK(cudaMemcpyAsync(hraw, raw, 32, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             const uint64_t t1 = now_ns();
-            if (i >= 0) t.push_back((t1 - t0) * 1e-9);
-            cs = hraw[0];
+            if (i >= 0) times[j].push_back((t1 - t0) * 1e-9);
+            sums[j] = hraw[0];
         }
+    }
+    for (int j = 0; j < nk; ++j) {
+        const auto& k = kernels[j];
+        const std::vector<double>& t = times[j];
+        const uint64_t cs = sums[j];
         double m = 0, v = 0;
         for (double x : t) m += x;
         m /= t.size();
         for (double x : t) v += (x - m) * (x - m);
         v /= t.size();
-        Stat q{m, std::sqrt(v), *std::min_element(t.begin(), t.end()), *std::max_element(t.begin(), t.end()), cs};
+        std::vector<double> srt = t;
+        std::sort(srt.begin(), srt.end());
+        const double med = srt[srt.size() / 2];
+        std::vector<double> dev;
+        for (double x : t) dev.push_back(std::fabs(x - med));
+        std::sort(dev.begin(), dev.end());
+        Stat q{m, std::sqrt(v), srt.front(), srt.back(), med, dev[dev.size() / 2], cs, t};
         st.push_back(q);
         printf("{\"kernel\": \"%s\", \"extra_instr\": %d, \"every_rounds\": %d, \"runs\": %d, \"t_avg_s\": %.6f, "
-               "\"sigma_s\": %.6f, \"t_min_s\": %.6f, \"t_max_s\": %.6f, \"threshold_s\": %.6f, \"checksum\": \"0x%016llx\"}\n",
-               k.name, k.extra, k.every, runs, q.avg, q.sd, q.mn, q.mx, q.avg + 2.5 * q.sd, (unsigned long long)cs);
+               "\"sigma_s\": %.6f, \"t_min_s\": %.6f, \"t_med_s\": %.6f, \"t_max_s\": %.6f, \"threshold_s\": %.6f, "
+               "\"checksum\": \"0x%016llx\"}\n",
+               k.name, k.extra, k.every, runs, q.avg, q.sd, q.mn, q.med, q.mx, q.avg + 2.5 * q.sd, (unsigned long long)cs);
         fflush(stdout);
     }
     // verdicts: adversary vs the honest kernel with the same unroll
@@ -109,11 +128,21 @@ int main(int argc, char** argv) {
     for (auto& p : pairs) {
         const Stat& hs = st[p[0]];
         const Stat& as = st[p[1]];
-        const double thr = hs.avg + 2.5 * hs.sd;
-        printf("{\"summary\": \"%s vs %s\", \"honest_t_avg_s\": %.6f, \"honest_sigma_s\": %.6f, \"threshold_s\": %.6f, "
-               "\"adversary_t_min_s\": %.6f, \"slowdown\": %.5f, \"detected\": %s, \"same_checksum\": %s}\n",
-               kernels[p[1]].name, kernels[p[0]].name, hs.avg, hs.sd, thr, as.mn, as.avg / hs.avg - 1.0,
-               as.mn > thr ? "true" : "false", hs.cs == as.cs ? "true" : "false");
+        const double thr = hs.avg + 2.5 * hs.sd;                      // the paper's rule
+        const double rthr = hs.med + 2.5 * 1.4826 * hs.mad;           // robust variant (median + 2.5 sigma_MAD)
+        auto frac_above = [](const std::vector<double>& xs, double th) {
+            size_t c = 0;
+            for (double x : xs) c += x > th;
+            return double(c) / xs.size();
+        };
+        printf("{\"summary\": \"%s vs %s\", \"rounds\": %u, \"honest_t_avg_s\": %.6f, \"honest_sigma_s\": %.6f, "
+               "\"threshold_s\": %.6f, \"adversary_t_min_s\": %.6f, \"adversary_t_med_s\": %.6f, \"slowdown\": %.5f, "
+               "\"detected_tmin_gt_threshold\": %s, \"honest_rejected_frac\": %.3f, \"adversary_rejected_frac\": %.3f, "
+               "\"robust_threshold_s\": %.6f, \"robust_honest_rejected_frac\": %.3f, \"robust_adversary_rejected_frac\": %.3f, "
+               "\"same_checksum\": %s}\n",
+               kernels[p[1]].name, kernels[p[0]].name, rounds, hs.avg, hs.sd, thr, as.mn, as.med, as.med / hs.med - 1.0,
+               as.mn > thr ? "true" : "false", frac_above(hs.t, thr), frac_above(as.t, thr), rthr,
+               frac_above(hs.t, rthr), frac_above(as.t, rthr), hs.cs == as.cs ? "true" : "false");
     }
     return 0;
 }

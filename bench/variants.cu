@@ -31,8 +31,11 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; };
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 1, 1),
-    VARL(1, 0), VARL(1, 1), VARL(1, 3), VARL(1, 4), VARL(4, 0), VARL(4, 3), VARL(4, 4), VARL(8, 0), VARL(8, 3), VARL(8, 4),
+    VARA(1, true, false, 0, 1, 1), VARA(1, true, false, 0, 8, 1), VARA(1, true, false, 0, 16, 1),
+    VARA(1, true, false, 0, 24, 1), VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 64, 1),
+    VARA(4, true, false, 0, 1, 1), VARA(4, true, false, 0, 2, 1), VARA(4, true, false, 0, 4, 1), VARA(4, true, false, 0, 16, 1),
+    VAR(1, true, true, 0, 1), VAR(1, true, true, 0, 16),
+    VAR(1, false, true, 0, 1), VAR(1, false, true, 0, 16), VAR(4, false, true, 0, 1), VAR(4, false, true, 0, 16),
 };
 
 int main(int argc, char** argv) {

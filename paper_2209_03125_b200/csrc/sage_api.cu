@@ -46,14 +46,31 @@ using KernelFn = void (*)(const sage::KernelArgs);
 // Kernel variant per (P, placement, straddle).  Lowering choices measured on
 // B200 with bench/variants.cu: SMEM picks address
 // shared memory through an IMAD (ADDR=1) unless chunk addresses straddle a
-// 4 GiB boundary; GLOBAL picks use L1-allocating read-only loads.
+// 4 GiB boundary; GLOBAL picks use L1-allocating read-only loads.  The round
+// loop is unrolled "until it is not possible to unroll further without
+// causing instruction cache misses": 32 rounds (a 32 KiB loop body)
+// for P=1 from SMEM, 64 is slower; fewer where more unrolling spills.
+template <int P> struct Unroll;
+template <> struct Unroll<1> { static constexpr int smem = 32, smem_straddle = 16, global = 16; };
+template <> struct Unroll<4> { static constexpr int smem = 2, smem_straddle = 2, global = 16; };
+template <> struct Unroll<8> { static constexpr int smem = 1, smem_straddle = 1, global = 1; };
+
 template <int P>
 KernelFn kernel_for_p(bool smem, bool straddle) {
     if (smem) {
-        return straddle ? sage::sage_checksum_kernel<P, true, true, 0, 1, 0, 0>
-                        : sage::sage_checksum_kernel<P, true, false, 0, 1, 1, 0>;
+        return straddle ? sage::sage_checksum_kernel<P, true, true, 0, Unroll<P>::smem_straddle, 0, 0>
+                        : sage::sage_checksum_kernel<P, true, false, 0, Unroll<P>::smem, 1, 0>;
     }
-    return sage::sage_checksum_kernel<P, false, true, 0, 1, 0, 0>;
+    return sage::sage_checksum_kernel<P, false, true, 0, Unroll<P>::global, 0, 0>;
+}
+
+KernelFn kernel_for(uint32_t P, bool smem, bool straddle) {
+    switch (P) {
+        case 1: return kernel_for_p<1>(smem, straddle);
+        case 4: return kernel_for_p<4>(smem, straddle);
+        case 8: return kernel_for_p<8>(smem, straddle);
+        default: return nullptr;
+    }
 }
 
 // Inclusion-experiment variant (counts reads per chunk); GLOBAL placement.
@@ -62,15 +79,6 @@ KernelFn counting_kernel_for(uint32_t P) {
         case 1: return sage::sage_checksum_kernel<1, false, true, 0, 1, 0, 0, 0, true>;
         case 4: return sage::sage_checksum_kernel<4, false, true, 0, 1, 0, 0, 0, true>;
         case 8: return sage::sage_checksum_kernel<8, false, true, 0, 1, 0, 0, 0, true>;
-        default: return nullptr;
-    }
-}
-
-KernelFn kernel_for(uint32_t P, bool smem, bool straddle) {
-    switch (P) {
-        case 1: return kernel_for_p<1>(smem, straddle);
-        case 4: return kernel_for_p<4>(smem, straddle);
-        case 8: return kernel_for_p<8>(smem, straddle);
         default: return nullptr;
     }
 }
