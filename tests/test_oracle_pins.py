@@ -327,3 +327,53 @@ def test_address_formula_identity():
         C = int(rng.integers(0, 2**32))
         W = 1 << int(rng.integers(0, 20))
         assert (4 * C) % (4 * W) == 4 * (C % W) == 4 * (C & (W - 1))
+
+
+def test_nonce_is_added_to_the_splitmix_counter():
+    """I1 adds the nonce to the counter (g+1)*G: nonce = G makes thread 0 start
+    from SplitMix64 output #2 of seed 0, 0x6E789E6AA1B965F4 (published); an XOR
+    would give sm(0) instead."""
+    a, _ = oracle.thread_init(GAMMA, 0)
+    assert a[0] == ((oracle.xs(0x6E789E6AA1B965F4) * XS_MULT_DEC) & M64) >> 32
+
+
+def test_zero_seed_maps_to_gamma():
+    """I2: the only zero SplitMix64 output is sm(0) = 0 (the finaliser fixes 0),
+    reached for nonce = -(g+1)*G; the xorshift state then starts at G."""
+    assert oracle.splitmix_mix(0) == 0
+    nonce = (-GAMMA) & M64                      # thread g = 0
+    a, x = oracle.thread_init(nonce, 0)
+    xs = GAMMA
+    for j in range(16):
+        xs = oracle.xs(xs)
+        assert a[j] == ((xs * XS_MULT_DEC) & M64) >> 32
+    assert x == xs
+
+
+def test_all_sixteen_seed_words():
+    """I3: a[j] = hi32(x_j * M64) for the j-th xorshift state after the seed."""
+    a, x = oracle.thread_init(0, 5)            # thread 5: SplitMix64 output #6 of seed 0
+    s = oracle.splitmix_mix((6 * GAMMA) & M64)
+    for j in range(16):
+        s = oracle.xs(s)
+        assert a[j] == ((s * XS_MULT_DEC) & M64) >> 32
+    assert x == s
+
+
+def test_data_pointer_scales_with_pick_words():
+    """R5: dp = base + 4*P*i.  Region chunk k holds word value k in every word;
+    a = 0 except a[15] = C fixes i, base 0: a[0]' = R6 fold of t0 = lo32(y) + 4*P*i."""
+    for P in (4, 8):
+        nc = 64
+        words = np.repeat(np.arange(nc, dtype=np.uint32), P)
+        region = words.view(np.uint8)
+        for C in (0, 0x1234567, 0xFFFFFFFF):
+            A, X = _zero_state()
+            A[:, 15] = C
+            A2, _ = oracle.warp_rounds(A, X, region, 0, 0, 1, P=P)
+            y = (0x2000001 * XS_MULT_DEC) & M64
+            i = ((y >> 32) ^ C) & (nc - 1)
+            t = ((y & M32) + 4 * P * i) & M32
+            for _ in range(P):
+                t = (rotl(t, 5) + i) & M32
+            assert int(A2[0, 0]) == t, (P, C)
