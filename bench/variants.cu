@@ -22,20 +22,19 @@
     } while (0)
 
 using Fn = void (*)(const sage::KernelArgs);
-struct V { const char* name; Fn fn; int P; bool smem; bool straddle; };
+struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; };
 
 #define VAR(P, S, ST, XS, U) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U>, P, S, ST}
 #define VARL(P, LD) {"P" #P " global ld" #LD, sage::sage_checksum_kernel<P, false, true, 0, 1, 0, LD>, P, false, true}
+#define VARI(P, U, A, ILP) {"P" #P " smem straddlefalse unroll" #U " addr" #A " ILP" #ILP, \
+                           sage::sage_checksum_kernel<P, true, false, 0, U, A, 0, 0, false, 0, ILP>, P, true, false, ILP}
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 1, 1), VARA(1, true, false, 0, 8, 1), VARA(1, true, false, 0, 16, 1),
-    VARA(1, true, false, 0, 24, 1), VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 64, 1),
-    VARA(4, true, false, 0, 1, 1), VARA(4, true, false, 0, 2, 1), VARA(4, true, false, 0, 4, 1), VARA(4, true, false, 0, 16, 1),
-    VAR(1, true, true, 0, 1), VAR(1, true, true, 0, 16),
-    VAR(1, false, true, 0, 1), VAR(1, false, true, 0, 16), VAR(4, false, true, 0, 1), VAR(4, false, true, 0, 16),
+    VARA(1, true, false, 0, 32, 1), VARI(1, 1, 1, 2), VARI(1, 4, 1, 2), VARI(1, 8, 1, 2), VARI(1, 16, 1, 2),
+    VARI(1, 8, 2, 2), VARA(4, true, false, 0, 2, 2), VARI(4, 1, 2, 2), VARI(4, 4, 2, 2),
 };
 
 int main(int argc, char** argv) {
@@ -84,7 +83,7 @@ int main(int argc, char** argv) {
         for (int rep = 0; rep < 3; ++rep) {
             CK(cudaMemset(raw, 0, 32));
             CK(cudaEventRecord(e0));
-            v.fn<<<blocks, threads, v.smem ? bytes : 0>>>(a);
+            v.fn<<<blocks / v.ilp, threads, v.smem ? bytes : 0>>>(a);
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             CK(cudaGetLastError());

@@ -182,7 +182,9 @@ struct KernelArgs {
     uint32_t p2[3];
     uint32_t four_p;          // 4*P as a runtime value (forces IMAD for the chunk offset)
     uint32_t zero;            // 0; operand of the injected instructions of EXTRA > 0 (timing adversary)
+    uint32_t one;             // 1; multiplier that keeps an add on the FMA pipe (ADDR = 2)
     uint32_t* counts;         // COUNT variant only: per-chunk read counters (inclusion experiment)
+    uint64_t* cta_trace;      // optional: per CTA {smid, start ns, end ns, clock64 span} (diagnostics)
 };
 
 // The region staged in shared memory (SMEM placement): namespace-scope so the
@@ -239,8 +241,8 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 //   EXTRA    number of result-neutral instructions injected (when `inject`) into
 //            the round (0 in the product; > 0 only for the timing-adversary
 //            experiment, the B200 analogue of Table 1 Exp 2's
-//            "adversarial NOP"; the kernel injects them in the first
-//            round of every UNROLL-round trip)
+//            "adversarial NOP"; the kernel injects them every EVERY
+//            rounds of the unrolled trip, or in its first round when EVERY = 0)
 //   COUNT    also count reads per chunk into args.counts (the memory-region
 //            inclusion experiment); not in the timed path
 template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false>
@@ -257,7 +259,13 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
     // R4, R5, R6 (first part)
     Pick<P> d;
     uint32_t t;
-    if constexpr (SMEM && !STRADDLE && ADDR == 1) {
+    if constexpr (SMEM && !STRADDLE && ADDR == 2) {
+        // both chunk offsets and the R6 add as IMADs (FMA pipe), sparing the ALU pipe
+        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
+        const uint32_t lo_dp = i * args.four_p + static_cast<uint32_t>(base);
+        d = load_shared_addr<P>(addr);
+        t = ((static_cast<uint32_t>(y) ^ r) * args.one + lo_dp) ^ static_cast<uint32_t>(base >> 32);
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 1) {
         // shared-window address of the chunk on the FMA pipe; lo32(dp) = addr + (lo32(base) - smem)
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         d = load_shared_addr<P>(addr);
@@ -293,9 +301,14 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
     a[kAccum - 1] ^= __shfl_sync(0xFFFFFFFFu, t, src_lane);
 }
 
+//   ILP      logical SCS-1 warps per hardware warp: 1 = one lane state per
+//            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
+//            independent lane states per thread (interleaved by ptxas), one
+//            CTA x 1024 threads per SM at 64 registers -- the same register file
+//            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
-          bool COUNT = false>
-__global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs args) {
+          bool COUNT = false, int EVERY = 0, int ILP = 1>
+__global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint64_t t_start_ns;
@@ -329,19 +342,27 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
         }
     }
 
-    // a1: I1-I3
-    const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // a1: I1-I3.  Hardware warp hw computes the ILP logical SCS-1 warps
+    // hw*ILP .. hw*ILP+ILP-1 (lane l of each); logical thread g = 32*warp + l.
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t src_lane = (lane + 1u) & 31u;
-    uint64_t x = splitmix(args.nonce + (g + 1) * kGamma);
-    if (x == 0) x = kGamma;
-    uint32_t a[kAccum];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint64_t hw_warp = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+    uint32_t a[ILP][kAccum];
+    uint32_t xlo[ILP], xhi[ILP];
 #pragma unroll
-    for (int j = 0; j < kAccum; ++j) {
-        x = xorshift(x);
-        a[j] = static_cast<uint32_t>((x * kXsMult) >> 32);
+    for (int s = 0; s < ILP; ++s) {
+        const uint64_t g = (hw_warp * ILP + s) * 32u + lane;
+        uint64_t x = splitmix(args.nonce + (g + 1) * kGamma);
+        if (x == 0) x = kGamma;
+#pragma unroll
+        for (int j = 0; j < kAccum; ++j) {
+            x = xorshift(x);
+            a[s][j] = static_cast<uint32_t>((x * kXsMult) >> 32);
+        }
+        xlo[s] = static_cast<uint32_t>(x);
+        xhi[s] = static_cast<uint32_t>(x >> 32);
     }
-    uint32_t xlo = static_cast<uint32_t>(x), xhi = static_cast<uint32_t>(x >> 32);
 
     const uint64_t base = reinterpret_cast<uint64_t>(args.region);
     const uint32_t nc_mask = args.nc_mask;
@@ -354,27 +375,35 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
     const uint32_t main_end = rounds - rounds % UNROLL;
     for (; r < main_end; r += UNROLL) {
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a, xlo, xhi, r + u, base, nc_mask, src_lane, args, policy,
-                                                                  u == 0);
-    }
-    for (; r < rounds; ++r)
-        scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a, xlo, xhi, r, base, nc_mask, src_lane, args, policy, true);
-
-    // a11: F1-F2
-    uint32_t e = 0, o = 0;
+        for (int u = 0; u < UNROLL; ++u) {
 #pragma unroll
-    for (int j = 0; j < kAccum; j += 2) { e ^= a[j]; o ^= a[j + 1]; }
-    uint64_t f = ((static_cast<uint64_t>(o) << 32) | e) ^ ((static_cast<uint64_t>(xhi) << 32) | xlo);
-
-    // a12: warp -> block -> grid
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) f += __shfl_down_sync(0xFFFFFFFFu, f, off);
-    const uint32_t warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        red[warp] = f;
-        if (args.per_warp) args.per_warp[blockIdx.x * (blockDim.x >> 5) + warp] = f;
+            for (int s = 0; s < ILP; ++s)
+                scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(
+                    a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
+                    EVERY > 0 ? (u % EVERY == 0) : (u == 0));
+        }
     }
+    for (; r < rounds; ++r) {
+#pragma unroll
+        for (int s = 0; s < ILP; ++s)
+            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
+                                                                      args, policy, true);
+    }
+
+    // a11: F1-F2, a12: warp -> block -> grid
+    uint64_t fw = 0;
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) {
+        uint32_t e = 0, o = 0;
+#pragma unroll
+        for (int j = 0; j < kAccum; j += 2) { e ^= a[s][j]; o ^= a[s][j + 1]; }
+        uint64_t f = ((static_cast<uint64_t>(o) << 32) | e) ^ ((static_cast<uint64_t>(xhi[s]) << 32) | xlo[s]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) f += __shfl_down_sync(0xFFFFFFFFu, f, off);
+        if (lane == 0 && args.per_warp) args.per_warp[hw_warp * ILP + s] = f;
+        fw += f;
+    }
+    if (lane == 0) red[warp] = fw;
     __syncthreads();
     if (warp == 0) {
         const uint32_t nw = blockDim.x >> 5;
@@ -392,6 +421,15 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
                       static_cast<unsigned long long>(~t_start_ns));
             atomicMax(reinterpret_cast<unsigned long long*>(&args.raw[3]),
                       static_cast<unsigned long long>(t_end_ns));
+            if (args.cta_trace) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                uint64_t* tr = args.cta_trace + 4ull * blockIdx.x;
+                tr[0] = smid;
+                tr[1] = t_start_ns;
+                tr[2] = t_end_ns;
+                tr[3] = static_cast<uint64_t>(c_end - c_start);
+            }
         }
     }
 }
@@ -400,6 +438,7 @@ __global__ void __launch_bounds__(1024, 2) sage_checksum_kernel(const KernelArgs
 inline void fill_tables(KernelArgs& args, uint32_t P) {
     args.four_p = 4u * P;
     args.zero = 0;
+    args.one = 1;
     for (int j = 0; j < kAccum; ++j) args.mul[j] = mul_of(j);
     args.p2[0] = 1u << 20;
     args.p2[1] = 1u << 25;
