@@ -48,6 +48,34 @@ def calibrate(samples, k=THRESHOLD_SIGMAS, min_runs=30):
     return TimingModel(t_avg=mean, sigma=math.sqrt(var), runs=n, k=k)
 
 
+def calibrate_quantile(samples, q=0.99, min_runs=30):
+    """Empirical-quantile timing model ("an empirical-quantile threshold
+    mode since ... noise need not be normal"): threshold = the q-quantile of the
+    honest calibration times (linear interpolation).  t_avg / sigma are still
+    reported; k is NaN because the threshold is not t_avg + k*sigma."""
+    xs = [float(s) for s in samples]
+    if len(xs) < min_runs:
+        raise ValueError("calibration needs >= %d runs, got %d" % (min_runs, len(xs)))
+    if not 0.0 < q < 1.0:
+        raise ValueError("q must be in (0, 1)")
+    base = calibrate(xs, min_runs=min_runs)
+    return QuantileTimingModel(t_avg=base.t_avg, sigma=base.sigma, runs=base.runs, q=q,
+                               quantile=percentile(xs, 100.0 * q))
+
+
+@dataclass(frozen=True)
+class QuantileTimingModel:
+    t_avg: float
+    sigma: float
+    runs: int
+    q: float
+    quantile: float
+
+    @property
+    def threshold(self):
+        return self.quantile
+
+
 class NonceLedger:
     """Tracks nonces already used in a session."""
 

@@ -81,3 +81,20 @@ def test_normal_tail():
 def test_percentile():
     assert V.percentile([1, 2, 3, 4, 5], 50) == 3
     assert V.percentile(list(range(101)), 99) == pytest.approx(99)
+
+
+def test_quantile_calibration():
+    """S:311 empirical-quantile mode: a bimodal honest distribution (99% main
+    mode, 1% slow mode) keeps a tight threshold, unlike T_avg + 2.5 sigma."""
+    main = [1.0 + 1e-5 * (k % 7) for k in range(990)]
+    slow = [1.03] * 10
+    xs = main + slow
+    qm = V.calibrate_quantile(xs, q=0.98)
+    nm = V.calibrate(xs)
+    assert qm.threshold < 1.0001 < nm.threshold
+    adv = 1.0035                                  # +0.35% adversary
+    assert not V.verify(1, adv, 1, qm).accepted
+    assert V.verify(1, adv, 1, nm).accepted
+    assert V.verify(1, 1.00003, 1, qm).accepted
+    with pytest.raises(ValueError):
+        V.calibrate_quantile(xs, q=1.5)
