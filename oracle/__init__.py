@@ -18,15 +18,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sage_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "sha256_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force=False):
     """Compile sage_oracle.c with gcc -O2 (plain scalar, no -march)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
         tmp = _LIB + ".%d.tmp" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", tmp] + _SRCS)
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -49,6 +50,8 @@ def lib():
         L.sage_oracle_warp_rounds.argtypes = [p, p, p, u64, u64, u64, u64, ctypes.c_uint]
         L.sage_oracle_warp.restype = ctypes.c_int
         L.sage_oracle_warp.argtypes = [u64, p, u64, u64, u64, u64, ctypes.c_uint, p]
+        L.sage_oracle_sha256.restype = None
+        L.sage_oracle_sha256.argtypes = [p, u64, p, u64, p]
         L.sage_oracle_attest.restype = ctypes.c_int
         L.sage_oracle_attest.argtypes = [u64, p, u64, u64, u64, u64, u64, ctypes.c_uint, p]
         _lib = L
@@ -110,6 +113,19 @@ def attest(nonce, region, base, rounds, blocks, threads, P=1):
     if rc != 0:
         raise ValueError("oracle rejected arguments")
     return out.value
+
+
+def sha256(r, code):
+    """SHA-256(r || code) (SAGE Eq. (9)) from the plain C oracle; r, code bytes-like
+    or uint8 ndarrays."""
+    rb = np.frombuffer(bytes(r), dtype=np.uint8) if not isinstance(r, np.ndarray) else r.view(np.uint8).reshape(-1)
+    cb = np.frombuffer(bytes(code), dtype=np.uint8) if not isinstance(code, np.ndarray) else code.view(np.uint8).reshape(-1)
+    rb = np.ascontiguousarray(rb)
+    cb = np.ascontiguousarray(cb)
+    out = np.zeros(32, dtype=np.uint8)
+    lib().sage_oracle_sha256(rb.ctypes.data_as(ctypes.c_void_p), rb.nbytes, cb.ctypes.data_as(ctypes.c_void_p),
+                             cb.nbytes, out.ctypes.data_as(ctypes.c_void_p))
+    return out.tobytes()
 
 
 # ---- multi-process driver for large configs (one warp range per task) ----------

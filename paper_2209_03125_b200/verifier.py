@@ -51,8 +51,8 @@ def calibrate(samples, k=THRESHOLD_SIGMAS, min_runs=30):
 def calibrate_quantile(samples, q=0.99, min_runs=30):
     """Empirical-quantile timing model ("an empirical-quantile threshold
     mode since ... noise need not be normal"): threshold = the q-quantile of the
-    honest calibration times (linear interpolation).  t_avg / sigma are still
-    reported; k is NaN because the threshold is not t_avg + k*sigma."""
+    honest calibration times (linear interpolation).  t_avg and sigma are still
+    reported for context; the threshold does not depend on them."""
     xs = [float(s) for s in samples]
     if len(xs) < min_runs:
         raise ValueError("calibration needs >= %d runs, got %d" % (min_runs, len(xs)))
