@@ -116,6 +116,16 @@ int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
 int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
                          uint64_t rounds, uint32_t* counts_out, sage_result* out);
 
+/* User-kernel authenticity check, SAGE Eq. (9): h = SHA-256(r || code)
+ * computed on the GPU over `code_len` bytes of DEVICE memory at `code` (the user
+ * kernel as located on the device) prefixed with the verifier's random value r
+ * (HOST pointer, r_len <= 128 bytes; SPEC S:367 uses 32).  Synchronous; writes
+ * the 32-byte big-endian digest to h_out (host) and, if non-NULL, the host wall
+ * time of the call to *elapsed_ns.  SAGE_EINVAL: r_len > 128, NULL h_out, NULL
+ * r or code with a non-zero length. */
+int sage_kernel_hash(sage_ctx* ctx, const uint8_t* r, size_t r_len, const void* code, size_t code_len,
+                     uint8_t* h_out, uint64_t* elapsed_ns);
+
 /* Decode a raw 4 x u64 result (host copy) into checksum / cycles / device_ns. */
 int sage_decode_raw(const uint64_t raw[4], sage_result* out);
 

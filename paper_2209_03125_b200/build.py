@@ -13,7 +13,8 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsage.so")
 CUBIN = os.path.join(PKG, "sage_kernel.cubin")
 SOURCES = [os.path.join(CSRC, "sage_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "sage_kernel.cuh"), os.path.join(INCLUDE, "sage.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "sage_kernel.cuh"), os.path.join(CSRC, "sage_hash.cuh"),
+                  os.path.join(INCLUDE, "sage.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-I" + INCLUDE, "-I" + CSRC]

@@ -11,6 +11,7 @@
 #include <new>
 
 #include "sage.h"
+#include "sage_hash.cuh"
 #include "sage_kernel.cuh"
 
 namespace {
@@ -286,6 +287,31 @@ int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size
     rc = attest_device(ctx, nonce, region, region_bytes, rounds, nullptr, &tmp, nullptr, counts_out);
     if (rc) return rc;
     *out = tmp;
+    return SAGE_OK;
+}
+
+int sage_kernel_hash(sage_ctx* ctx, const uint8_t* r, size_t r_len, const void* code, size_t code_len,
+                     uint8_t* h_out, uint64_t* elapsed_ns) {
+    if (ctx == nullptr || h_out == nullptr || (r == nullptr && r_len) || (code == nullptr && code_len))
+        return fail(SAGE_EINVAL, "null pointer%s");
+    if (r_len > static_cast<size_t>(sage::kHashRMax)) return fail(SAGE_EINVAL, "r longer than %s bytes", "128");
+    int rc = set_device(ctx);
+    if (rc) return rc;
+    sage::HashArgs args{};
+    args.code = static_cast<const uint8_t*>(code);
+    args.code_len = code_len;
+    args.out = reinterpret_cast<uint8_t*>(ctx->d_raw);
+    args.r_len = static_cast<uint32_t>(r_len);
+    if (r_len) memcpy(args.r, r, r_len);
+    const uint64_t t0 = now_ns();
+    sage::sage_sha256_kernel<<<1, 64, 0, ctx->stream>>>(args);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches++;
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_raw, ctx->d_raw, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const uint64_t t1 = now_ns();
+    memcpy(h_out, ctx->h_raw, 32);
+    if (elapsed_ns) *elapsed_ns = t1 - t0;
     return SAGE_OK;
 }
 

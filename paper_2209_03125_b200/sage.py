@@ -21,7 +21,7 @@ PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto"}
 
 # every symbol include/sage.h declares
 EXPORTS = ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
-           "sage_attest_host", "sage_attest_coverage", "sage_host_region_va", "sage_placement_for", "sage_query", "sage_launch_count",
+           "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va", "sage_placement_for", "sage_query", "sage_launch_count",
            "sage_stream", "sage_checksum_destroy", "sage_strerror", "sage_last_error")
 
 
@@ -73,6 +73,7 @@ def load(path=LIB):
     L.sage_attest_async.argtypes = [p, u64, p, sz, u64, p, p]
     L.sage_decode_raw.argtypes = [p, ctypes.POINTER(sage_result)]
     L.sage_attest_coverage.argtypes = [p, u64, p, sz, u64, p, ctypes.POINTER(sage_result)]
+    L.sage_kernel_hash.argtypes = [p, p, sz, p, sz, p, ctypes.POINTER(u64)]
     L.sage_attest_host.argtypes = [p, u64, p, sz, u64, ctypes.POINTER(sage_result)]
     L.sage_host_region_va.argtypes = [p, sz, ctypes.POINTER(u64)]
     L.sage_placement_for.argtypes = [p, sz, ctypes.POINTER(ctypes.c_uint32)]
@@ -88,8 +89,8 @@ def load(path=LIB):
     L.sage_last_error.argtypes = []
     L.sage_last_error.restype = ctypes.c_char_p
     for name in ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
-                 "sage_attest_coverage",
-                 "sage_attest_host", "sage_attest_coverage", "sage_host_region_va", "sage_placement_for", "sage_query"):
+                 "sage_attest_coverage", "sage_kernel_hash",
+                 "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va", "sage_placement_for", "sage_query"):
         getattr(L, name).restype = i
     _lib = L
     return L
@@ -172,6 +173,18 @@ def attest_coverage(ctx, nonce, region, rounds, counts_out, nbytes=None):
     return out
 
 
+def kernel_hash(ctx, r, code, nbytes=None):
+    """h = SHA-256(r || code) on the GPU (SAGE Eq. (9)); r: host bytes (<= 128),
+    code: device tensor / address.  Returns (digest bytes, elapsed_ns)."""
+    rb = bytes(r)
+    rbuf = ctypes.create_string_buffer(rb, len(rb)) if rb else None
+    out = ctypes.create_string_buffer(32)
+    ns = ctypes.c_uint64()
+    n = _nbytes(code, nbytes) if code is not None else 0
+    _check(load().sage_kernel_hash(ctx, rbuf, len(rb), _ptr(code) if n else None, n, out, ctypes.byref(ns)))
+    return out.raw, ns.value
+
+
 def decode_raw(raw4):
     """raw4: host sequence of 4 u64 (e.g. raw_out.cpu())."""
     arr = (ctypes.c_uint64 * 4)(*[int(v) & (2**64 - 1) for v in raw4])
@@ -243,6 +256,9 @@ class Context:
 
     def attest_coverage(self, nonce, region, rounds, counts_out, nbytes=None):
         return attest_coverage(self.ctx, nonce, region, rounds, counts_out, nbytes)
+
+    def kernel_hash(self, r, code, nbytes=None):
+        return kernel_hash(self.ctx, r, code, nbytes)
 
     def attest_host(self, nonce, host_region, rounds, nbytes=None):
         return attest_host(self.ctx, nonce, host_region, rounds, nbytes)
