@@ -296,3 +296,44 @@ def test_p8_auto_placement_is_global(dev):
         assert ctx.placement_for(8192) == sage.SAGE_GLOBAL
         res = ctx.attest(0x88, d, 250)
     assert res.checksum == oracle.attest(0x88, region, d.data_ptr(), 250, 2, 96, 8)
+
+
+def test_async_attestation_in_cuda_graph(dev):
+    """sage_attest_async is capturable: a CUDA graph of zero-fill + attestation,
+    replayed twice, reproduces the synchronous checksum."""
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    s = torch.cuda.Stream()
+    raw = torch.zeros(4, dtype=torch.int64, device=dev)
+    with sage.Context(blocks=4, threads=256, stream=s) as ctx:
+        ctx.attest(1, d, 10)                                  # warm the kernel / attributes outside capture
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            raw.zero_()
+            ctx.attest_async(0x6A, d, 500, raw)
+        for _ in range(2):
+            g.replay()
+            s.synchronize()
+            got = sage.decode_raw([int(v) for v in raw.cpu().tolist()]).checksum
+            assert got == oracle.attest(0x6A, region, d.data_ptr(), 500, 4, 256, 1)
+
+
+def test_two_contexts_on_concurrent_streams(dev):
+    """Independent contexts on their own streams (e.g. two verifier sessions)
+    give the same results as serial runs."""
+    import threading
+    region = make_region(4096, fill_seed=77)
+    d, _keep = to_dev(region, dev)
+    want = {n: oracle.attest(n, region, d.data_ptr(), 300, 2, 128, 1) for n in (101, 202)}
+    got = {}
+
+    def run(n):
+        with sage.Context(blocks=2, threads=128) as ctx:
+            got[n] = ctx.attest(n, d, 300).checksum
+
+    ts = [threading.Thread(target=run, args=(n,)) for n in want]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert got == want

@@ -1,0 +1,74 @@
+"""Build evidence from the compiled library (no GPU needed): the checksum
+kernels are sm_100a SASS, stage the region with the TMA bulk-copy engine
+(UBLKCP + mbarrier SYNCS), run R7 as IMAD + LEA.HI pairs, exchange through
+SHFL.IDX, and fit 32 registers (2 x 1024 threads per SM)."""
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_2209_03125_b200 import build
+
+pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not available")
+
+
+@pytest.fixture(scope="module")
+def sass():
+    lib = build.build()
+    return subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
+
+
+@pytest.fixture(scope="module")
+def res_usage():
+    lib = build.build()
+    return subprocess.run(["cuobjdump", "-res-usage", lib], capture_output=True, text=True, check=True).stdout
+
+
+def _functions(sass):
+    parts = re.split(r"\n\s+Function : ", sass)
+    return {p.split("\n", 1)[0].strip(): p for p in parts[1:]}
+
+
+def test_arch_is_sm100a(sass):
+    assert "arch = sm_100a" in sass
+
+
+def test_smem_kernels_use_tma_bulk_copy(sass):
+    funcs = _functions(sass)
+    smem = [n for n in funcs if n.startswith("_ZN4sage20sage_checksum_kernelILi") and "ELb1E" in n.split("ILi", 1)[1][:6]]
+    assert smem, "no SMEM checksum kernels found"
+    for n in smem:
+        body = funcs[n]
+        assert "UBLKCP.S.G" in body, n
+        assert "SYNCS.ARRIVE.TRANS64" in body and "SYNCS.PHASECHK.TRANS64" in body, n
+
+
+def test_round_is_imad_leahi_and_shuffle(sass):
+    funcs = _functions(sass)
+    ks = [n for n in funcs if n.startswith("_ZN4sage20sage_checksum_kernel")]
+    assert len(ks) >= 9
+    for n in ks:
+        body = funcs[n]
+        assert "SHFL.IDX" in body, n
+        assert len(re.findall(r"\bLEA\.HI\b", body)) >= 16, n
+        assert len(re.findall(r"\bIMAD R\d+, R\d+, c\[0x0\]", body)) + \
+            len(re.findall(r"\bIMAD R\d+, R\d+, UR\d+", body)) >= 16, n
+
+
+def test_registers_allow_two_ctas_of_1024(res_usage):
+    regs = {}
+    name = None
+    for ln in res_usage.splitlines():
+        m = re.search(r"Function (\S+):", ln)
+        if m:
+            name = m.group(1)
+        m = re.search(r"REG:(\d+)", ln)
+        if m and name:
+            regs[name] = int(m.group(1))
+    ks = {n: r for n, r in regs.items() if n.startswith("_ZN4sage20sage_checksum_kernel")}
+    assert ks
+    for n, r in ks.items():
+        if n.endswith("ILi2EEEvNS_10KernelArgsE"):       # ILP=2 variants (not instantiated in the product)
+            continue
+        assert r <= 32, (n, r)
