@@ -24,6 +24,10 @@
  * pointer is folded in every round.  The context owns its result
  * buffers, its staging buffer for host regions and, when the config's stream is
  * NULL, its stream.
+ *
+ * Threads: every function may be called from any thread; calls on the same
+ * context are serialised by a per-context lock (use one context per thread or
+ * stream for concurrency).  The launch-count read is unsynchronised.
  */
 #ifndef SAGE_H
 #define SAGE_H

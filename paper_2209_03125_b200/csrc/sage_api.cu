@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 
 #include "sage.h"
@@ -99,6 +100,7 @@ struct sage_ctx {
     void* d_stage = nullptr;        // device copy of a host region (sage_attest_host)
     size_t stage_bytes = 0;
     uint64_t launches = 0;
+    std::mutex mu;                  // serialises calls that use the ctx-owned buffers
 };
 
 namespace {
@@ -258,6 +260,7 @@ int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     int rc = validate(ctx, region, region_bytes, rounds);
     if (rc) return rc;
     if (out == nullptr) return fail(SAGE_EINVAL, "out is null%s");
+    std::lock_guard<std::mutex> lock(ctx->mu);
     sage_result tmp;
     rc = attest_device(ctx, nonce, region, region_bytes, rounds, per_warp_out, &tmp, nullptr);
     if (rc) return rc;
@@ -270,6 +273,7 @@ int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     int rc = validate(ctx, region, region_bytes, rounds);
     if (rc) return rc;
     if (raw_out == nullptr) return fail(SAGE_EINVAL, "raw_out is null%s");
+    std::lock_guard<std::mutex> lock(ctx->mu);
     rc = set_device(ctx);
     if (rc) return rc;
     return launch(ctx, nonce, region, region_bytes, rounds, raw_out, per_warp_out, nullptr);
@@ -280,6 +284,7 @@ int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size
     int rc = validate(ctx, region, region_bytes, rounds);
     if (rc) return rc;
     if (counts_out == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    std::lock_guard<std::mutex> lock(ctx->mu);
     rc = set_device(ctx);
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(counts_out, 0, region_bytes / (4ull * ctx->pick_words) * sizeof(uint32_t), ctx->stream));
@@ -295,6 +300,7 @@ int sage_kernel_hash(sage_ctx* ctx, const uint8_t* r, size_t r_len, const void* 
     if (ctx == nullptr || h_out == nullptr || (r == nullptr && r_len) || (code == nullptr && code_len))
         return fail(SAGE_EINVAL, "null pointer%s");
     if (r_len > static_cast<size_t>(sage::kHashRMax)) return fail(SAGE_EINVAL, "r longer than %s bytes", "128");
+    std::lock_guard<std::mutex> lock(ctx->mu);
     int rc = set_device(ctx);
     if (rc) return rc;
     sage::HashArgs args{};
@@ -328,6 +334,7 @@ int sage_decode_raw(const uint64_t raw[4], sage_result* out) {
 int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, size_t region_bytes, uint64_t rounds,
                      sage_result* out) {
     if (ctx == nullptr || host_region == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    std::lock_guard<std::mutex> lock(ctx->mu);
     int rc = set_device(ctx);
     if (rc) return rc;
     rc = ensure_stage(ctx, region_bytes ? region_bytes : 1);
@@ -343,6 +350,7 @@ int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, siz
 
 int sage_host_region_va(sage_ctx* ctx, size_t region_bytes, uint64_t* va_out) {
     if (ctx == nullptr || va_out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    std::lock_guard<std::mutex> lock(ctx->mu);
     int rc = set_device(ctx);
     if (rc) return rc;
     rc = ensure_stage(ctx, region_bytes ? region_bytes : 1);

@@ -337,3 +337,23 @@ def test_two_contexts_on_concurrent_streams(dev):
     for t in ts:
         t.join()
     assert got == want
+
+
+def test_one_context_shared_by_threads(dev):
+    """Calls on one context from several threads are serialised by its lock."""
+    import threading
+    region = make_region(4096, fill_seed=78)
+    d, _keep = to_dev(region, dev)
+    nonces_ = list(range(300, 308))
+    want = {n: oracle.attest(n, region, d.data_ptr(), 200, 1, 64, 1) for n in nonces_}
+    got = {}
+    with sage.Context(blocks=1, threads=64) as ctx:
+        def run(ns):
+            for n in ns:
+                got[n] = ctx.attest(n, d, 200).checksum
+        ts = [threading.Thread(target=run, args=(nonces_[k::4],)) for k in range(4)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    assert got == want
