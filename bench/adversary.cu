@@ -142,6 +142,7 @@ int main(int argc, char** argv) {
         std::vector<double> csrt = cal;
         std::sort(csrt.begin(), csrt.end());
         const double rthr = csrt[size_t(0.99 * (csrt.size() - 1))];
+        const double qthr = csrt[size_t(0.95 * (csrt.size() - 1))];   // restart policy threshold
         auto frac_above = [](const std::vector<double>& xs, double th) {
             size_t c = 0;
             for (double x : xs) c += x > th;
@@ -151,10 +152,12 @@ int main(int argc, char** argv) {
                "\"threshold_s\": %.6f, \"adversary_t_min_s\": %.6f, \"adversary_t_med_s\": %.6f, \"slowdown\": %.5f, "
                "\"detected_tmin_gt_threshold\": %s, \"honest_rejected_frac\": %.3f, \"adversary_rejected_frac\": %.3f, "
                "\"p99_threshold_s\": %.6f, \"p99_honest_rejected_frac\": %.3f, \"p99_adversary_rejected_frac\": %.3f, "
+               "\"p95_threshold_s\": %.6f, \"p95_honest_reject_per_try\": %.3f, \"p95_adversary_accept_per_try\": %.3f, "
                "\"same_checksum\": %s}\n",
                kernels[p[1]].name, kernels[p[0]].name, rounds, cm, cv, thr, as.mn, as.med, as.med / hs.med - 1.0,
                as.mn > thr ? "true" : "false", frac_above(held, thr), frac_above(as.t, thr), rthr,
-               frac_above(held, rthr), frac_above(as.t, rthr), hs.cs == as.cs ? "true" : "false");
+               frac_above(held, rthr), frac_above(as.t, rthr), qthr, frac_above(held, qthr), 1.0 - frac_above(as.t, qthr),
+               hs.cs == as.cs ? "true" : "false");
     }
     return 0;
 }

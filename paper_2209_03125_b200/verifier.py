@@ -104,6 +104,22 @@ def verify(response, elapsed, expected, model, nonce=None, ledger=None):
     return Verdict(True, "ok", elapsed, expected, response)
 
 
+def verify_with_restarts(attempt, model, max_tries=3, ledger=None):
+    """The paper's false-positive handling: "in which case the verification
+    process is restarted".  attempt() runs one attestation with a fresh
+    nonce and returns (nonce, response, elapsed, expected); the session is
+    accepted at the first attempt that verifies, rejected after max_tries.  A
+    wrong checksum or a reused nonce rejects immediately (only timeouts are
+    retried).  Returns (Verdict of the last attempt, attempts made)."""
+    v = None
+    for k in range(1, max_tries + 1):
+        nonce, response, elapsed, expected = attempt()
+        v = verify(response, elapsed, expected, model, nonce=nonce, ledger=ledger)
+        if v.accepted or v.reason != "timeout":
+            return v, k
+    return v, max_tries
+
+
 def inclusion_probability(words, accesses):
     """Probability that a given word is never read: (1 - 1/S)^N,
     evaluated as exp(N * log1p(-1/S)) for precision.  The paper prints 0.082

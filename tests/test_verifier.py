@@ -98,3 +98,17 @@ def test_quantile_calibration():
     assert V.verify(1, 1.00003, 1, qm).accepted
     with pytest.raises(ValueError):
         V.calibrate_quantile(xs, q=1.5)
+
+
+def test_verify_with_restarts():
+    """a timeout restarts with a fresh nonce; a wrong checksum does not."""
+    m = V.TimingModel(1.0, 0.01, 100)
+    seq = iter([(1, 5, 1.5, 5), (2, 5, 1.01, 5)])
+    v, k = V.verify_with_restarts(lambda: next(seq), m, max_tries=3, ledger=V.NonceLedger())
+    assert v.accepted and k == 2
+    seq = iter([(3, 5, 1.5, 5)] * 3)
+    v, k = V.verify_with_restarts(lambda: next(seq), m, max_tries=3)
+    assert not v.accepted and v.reason == "timeout" and k == 3
+    seq = iter([(4, 6, 0.9, 5), (5, 5, 0.9, 5)])
+    v, k = V.verify_with_restarts(lambda: next(seq), m)
+    assert not v.accepted and v.reason == "checksum_mismatch" and k == 1
