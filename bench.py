@@ -43,6 +43,8 @@ CONFIGS = {
     "c3p1": (256 << 20, 1, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=1, 1e4 rounds"),
     "c3p4": (256 << 20, 4, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=4, 1e4 rounds"),
     "c3p8": (256 << 20, 8, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=8, 1e4 rounds"),
+    "c3big": (2 << 30, 1, 10_000, "full occupancy, 2 GiB HBM region (GLOBAL), P=1, 1e4 rounds"),
+    "c3bigp8": (2 << 30, 8, 10_000, "full occupancy, 2 GiB HBM region (GLOBAL), P=8, 1e4 rounds"),
 }
 
 
