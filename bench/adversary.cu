@@ -43,6 +43,8 @@ static K kernels[] = {
     {"+1 instr / round", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 1, false, 1>, 1, 1},
     {"+1 instr / 8 rounds", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 1, false, 8>, 1, 8},
     {"+1 instr / 32 rounds", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 1, false, 32>, 1, 32},
+    {"+1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, -1, false, 1>, -1, 1},
+    {"+2 IMAD / round", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, -2, false, 1>, -2, 1},
 };
 
 static uint64_t now_ns() {
@@ -125,7 +127,7 @@ int main(int argc, char** argv) {
         fflush(stdout);
     }
     // verdicts: adversary vs the honest kernel with the same unroll
-    const int pairs[][2] = {{0, 1}, {0, 2}, {0, 3}};
+    const int pairs[][2] = {{0, 1}, {0, 2}, {0, 3}, {0, 4}, {0, 5}};
     for (auto& p : pairs) {
         const Stat& hs = st[p[0]];
         const Stat& as = st[p[1]];

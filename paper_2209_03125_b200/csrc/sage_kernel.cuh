@@ -292,8 +292,12 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
     }
     // injected adversary work: dependent ALU ops that leave t unchanged (t ^ 0)
     if (inject) {
+        // EXTRA > 0: dependent ALU-pipe ops (t ^ 0); EXTRA < 0: dependent FMA-pipe ops (t * 1)
 #pragma unroll
-        for (int e = 0; e < EXTRA; ++e) t ^= args.zero;
+        for (int e = 0; e < (EXTRA > 0 ? EXTRA : -EXTRA); ++e) {
+            if constexpr (EXTRA > 0) t ^= args.zero;
+            else t = t * args.one;
+        }
     }
     // R8
     t = t + (t >> (C & 31u));
