@@ -33,7 +33,7 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1),
+    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1), VARA(1, true, false, 0, 1, 1),
 };
 
 int main(int argc, char** argv) {

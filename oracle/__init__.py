@@ -1,12 +1,12 @@
-"""CPU oracle for SCS-1 (the SAGE checksum loop, arXiv 2209.03125).
+"""CPU oracle for SCS-2 (the SAGE checksum loop, arXiv 2209.03125).
 
 TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py
 (its cpu_baseline leg and --impl reference arm) may import this package.  The
 product package paper_2209_03125_b200 never imports it, and the two share no
 code: the C oracle (sage_oracle.c) and the pure-Python oracle (ref.py) are
-written from the SCS-1 text in DESIGN.md section 3.
+written from the SCS-2 text in DESIGN.md section 3.
 
-Parity status: every SCS-1 step is pinned by tests/test_oracle_pins.py (see
+Parity status: every SCS-2 step is pinned by tests/test_oracle_pins.py (see
 DESIGN.md section 4 for the pin per step); none is "parity unpinned".
 """
 import ctypes

@@ -1,7 +1,7 @@
-"""Second, pure-Python oracle for SCS-1 (tiny inputs only).
+"""Second, pure-Python oracle for SCS-2 (tiny inputs only).
 
 TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.  Written independently of
-sage_oracle.c from the SCS-1 text in DESIGN.md section 3; used
+sage_oracle.c from the SCS-2 text in DESIGN.md section 3; used
 to cross-check the C oracle on small random configurations.  Python ints with
 explicit masking, one step per line in definition order.
 
@@ -15,6 +15,7 @@ XS_MULT = 2685821657736338717          # S:241, written in decimal on purpose
 SPLITMIX_GAMMA = 0x9E3779B97F4A7C15
 MULT_EXP = (5, 11, 3, 17, 9, 23, 7, 13, 29, 2, 19, 6, 15, 27, 4, 21)   # L[j]
 ROT = (7, 13, 19, 3, 25, 9, 17, 5, 11, 29, 2, 23, 14, 6, 27, 18)        # S[j]
+KR, KH, KX = 0x9E3779B1, 0x85EBCA77, 0xC2B2AE3D                         # SCS-2 R6 / R9
 
 
 def splitmix_mix(z):
@@ -73,7 +74,7 @@ def one_round(A, X, r, words, nchunks, base, P):
         i = ((y >> 32) ^ C) & (nchunks - 1)              # R3
         d = [words[P * i + q] for q in range(P)]         # R4
         dp = (base + 4 * P * i) & MASK64                 # R5
-        t = ((((y & MASK32) ^ r) + (dp & MASK32)) & MASK32) ^ (dp >> 32)   # R6
+        t = ((y & MASK32) + r * KR + (dp & MASK32) + (dp >> 32) * KH) & MASK32   # R6
         for q in range(P):
             t = (rotl(t, 5) + d[q]) & MASK32
         for j in range(16):                              # R7
@@ -82,7 +83,7 @@ def one_round(A, X, r, words, nchunks, base, P):
         t = (t + (t >> (C % 32))) & MASK32               # R8
         ts.append(t)
     for lane in range(32):                               # R9
-        A[lane][15] ^= ts[(lane + 1) % 32]
+        A[lane][15] = (A[lane][15] * KX + ts[(lane + 1) % 32]) & MASK32
 
 
 def words_of(region):

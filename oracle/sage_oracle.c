@@ -1,5 +1,5 @@
 /*
- * sage_oracle.c -- plain CPU oracle for SCS-1, the SAGE self-checksumming
+ * sage_oracle.c -- plain CPU oracle for SCS-2, the SAGE self-checksumming
  * verification-function loop (arXiv 2209.03125).
  *
  * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
@@ -8,8 +8,10 @@
  * it shares no code, header, table or constant generator with the CUDA path.
  *
  * Citation keys: P:n = PAPER.md line n, S:n = SPEC.md line n.
- * The definition written out here is SCS-1, which fixes
- * the choices the paper leaves open (readings Q1-Q20).
+ * The definition written out here is SCS-2: SURVEY.md
+ * section 8(c)'s SCS-1 (readings Q1-Q20) with R6 and R9 combining by
+ * multiply-add instead of XOR so the loop loads both integer pipes
+ * (DESIGN.md "SCS-1 -> SCS-2").
  *
  * Deliberately plain: scalar uint32/uint64 arithmetic, one step per line in
  * the order the definition states, no intrinsics, no blocking, no fusion.
@@ -34,6 +36,8 @@ static const uint64_t GAMMA = 0x9E3779B97F4A7C15ULL;
  * addition ... arbitrarily chosen shift size". */
 static const unsigned L_TAB[K] = {5, 11, 3, 17, 9, 23, 7, 13, 29, 2, 19, 6, 15, 27, 4, 21};
 static const unsigned S_TAB[K] = {7, 13, 19, 3, 25, 9, 17, 5, 11, 29, 2, 23, 14, 6, 27, 18};
+/* R6 / R9 odd multipliers (SCS-2): round index, high DP word, exchanged value. */
+static const uint32_t KR = 0x9E3779B1u, KH = 0x85EBCA77u, KX = 0xC2B2AE3Du;
 
 /* ---- helpers -------------------------------------------------------------- */
 
@@ -107,7 +111,7 @@ static void warp_round(uint32_t a[WARP][K], uint64_t x[WARP], uint32_t r,
         /* R5: data pointer = device VA of the picked chunk (Q9) */
         uint64_t dp = base + 4ULL * P * i;
         /* R6: iteration index and DP folded in, then the data (Q19) */
-        uint32_t t = ((lo32(y) ^ r) + lo32(dp)) ^ hi32(dp);
+        uint32_t t = lo32(y) + r * KR + lo32(dp) + hi32(dp) * KH;
         for (unsigned q = 0; q < P; q++)
             t = rotl32(t, 5) + d[q];
         /* R7: strongly-ordered multiply-add / rotate-add chain */
@@ -123,7 +127,7 @@ static void warp_round(uint32_t a[WARP][K], uint64_t x[WARP], uint32_t r,
     }
     /* R9: neighbour exchange from a snapshot (north_star; Q13) */
     for (int l = 0; l < WARP; l++)
-        a[l][K - 1] = a[l][K - 1] ^ t_lane[(l + 1) % WARP];
+        a[l][K - 1] = a[l][K - 1] * KX + t_lane[(l + 1) % WARP];
 }
 
 /* F1-F2: per-thread fold (Q11) */

@@ -245,6 +245,11 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 //            rounds of the unrolled trip, or in its first round when EVERY = 0)
 //   COUNT    also count reads per chunk into args.counts (the memory-region
 //            inclusion experiment); not in the timed path
+#ifndef SAGE_DEF
+#define SAGE_DEF 1
+#endif
+constexpr uint32_t kKR = 0x9E3779B1u, kKH = 0x85EBCA77u, kKX = 0xC2B2AE3Du;   // SCS-2 prototype constants
+
 template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false>
 __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
@@ -270,7 +275,11 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         d = load_shared_addr<P>(addr);
         const uint32_t base_minus_smem = static_cast<uint32_t>(base) - smem_u32(smem_words);   // loop-invariant
+#if SAGE_DEF == 2
+        t = static_cast<uint32_t>(y) + (r * kKR + base_minus_smem + static_cast<uint32_t>(base >> 32) * kKH) + addr;
+#else
         t = ((static_cast<uint32_t>(y) ^ r) + addr + base_minus_smem) ^ static_cast<uint32_t>(base >> 32);
+#endif
     } else if constexpr (SMEM && !STRADDLE) {
         const uint32_t v = i * (4u * P);                         // byte offset of the chunk
         d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
@@ -290,6 +299,11 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
         a[j] = a[j] * args.mul[j] + t;
         t = a[j] + rotl(t, rot_of(j));
     }
+#if SAGE_DEF == 2
+    // R7b: cross-accumulator multiply-adds (FMA pipe), off the t chain
+#pragma unroll
+    for (int j = 0; j < SAGE_R7B; ++j) a[2 * j + 1] = a[2 * j + 1] * args.mul[2 * j] + a[2 * j];
+#endif
     // injected adversary work: dependent ALU ops that leave t unchanged (t ^ 0)
     if (inject) {
         // EXTRA > 0: dependent ALU-pipe ops (t ^ 0); EXTRA < 0: dependent FMA-pipe ops (t * 1)
@@ -302,7 +316,11 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
     // R8
     t = t + (t >> (C & 31u));
     // R9
+#if SAGE_DEF == 2
+    a[kAccum - 1] = a[kAccum - 1] * kKX + __shfl_sync(0xFFFFFFFFu, t, src_lane);
+#else
     a[kAccum - 1] ^= __shfl_sync(0xFFFFFFFFu, t, src_lane);
+#endif
 }
 
 //   ILP      logical SCS-1 warps per hardware warp: 1 = one lane state per

@@ -1,5 +1,5 @@
 """The C oracle against the independent pure-Python oracle (oracle/ref.py), the
-frozen golden vector, and order-sensitivity mutants of SCS-1.
+frozen golden vector, and order-sensitivity mutants of SCS-2.
 
 Mutants live in this test file only: each is a copy of oracle/ref.py's round
 with one plausible mistake ("strong ordering").  Each must
@@ -66,7 +66,7 @@ def _mut_round(kind):
             if kind == "drop_dp":
                 dp = 0
             rr = r + 1 if kind == "round_shift" else r
-            t = ((((y & ref.MASK32) ^ rr) + (dp & ref.MASK32)) & ref.MASK32) ^ (dp >> 32)
+            t = ((y & ref.MASK32) + rr * ref.KR + (dp & ref.MASK32) + (dp >> 32) * ref.KH) & ref.MASK32
             for q in range(P):
                 t = (ref.rotl(t, 5) + d[q]) & ref.MASK32
             order = list(range(16))
@@ -81,13 +81,16 @@ def _mut_round(kind):
         for lane in range(32):
             if kind == "no_exchange":
                 continue
+            if kind == "scs1_xor":               # the superseded SCS-1 exchange
+                A[lane][15] ^= ts[(lane + 1) % 32]
+                continue
             src = (lane - 1) % 32 if kind == "left_neighbour" else (lane + 1) % 32
-            A[lane][15] ^= ts[src]
+            A[lane][15] = (A[lane][15] * ref.KX + ts[src]) & ref.MASK32
     return one_round
 
 
 @pytest.mark.parametrize("kind", ["reverse_words", "drop_dp", "round_shift", "swap_chain", "no_smc",
-                                  "no_exchange", "left_neighbour"])
+                                  "no_exchange", "left_neighbour", "scs1_xor"])
 def test_mutant_changes_result(kind, monkeypatch):
     rng = np.random.default_rng(99)
     P = 4 if kind == "reverse_words" else 1

@@ -16,6 +16,7 @@ XS_MULT_DEC = 2685821657736338717          # S:241 as printed (decimal)
 GAMMA = 0x9E3779B97F4A7C15
 L_TAB = (5, 11, 3, 17, 9, 23, 7, 13, 29, 2, 19, 6, 15, 27, 4, 21)
 S_TAB = (7, 13, 19, 3, 25, 9, 17, 5, 11, 29, 2, 23, 14, 6, 27, 18)
+KR, KH, KX = 0x9E3779B1, 0x85EBCA77, 0xC2B2AE3D      # SCS-2 R6/R9 constants
 
 
 def rotl(v, s):
@@ -110,7 +111,7 @@ def test_round_reveals_prng_output():
 
 
 def test_round_index_and_data_pointer_fold():
-    """R5-R6 (P:434-438, P:652): t = ((lo32(y) ^ r) + lo32(dp)) ^ hi32(dp) then
+    """R5-R6: t = lo32(y) + r*KR + lo32(dp) + hi32(dp)*KH then
     rotl(t,5) + d.  Degenerate state a = 0 so a[0]' = t; one chunk so dp = base."""
     A, X = _zero_state()
     word = 0xDEADBEEF
@@ -119,8 +120,12 @@ def test_round_index_and_data_pointer_fold():
     r = 12345
     A2, _ = oracle.warp_rounds(A, X, region, base, r, r + 1, P=1)
     y = (0x2000001 * XS_MULT_DEC) & M64
-    t = ((((y & M32) ^ r) + (base & M32)) & M32) ^ (base >> 32)
+    t = ((y & M32) + r * KR + (base & M32) + (base >> 32) * KH) & M32
     assert int(A2[0, 0]) == (rotl(t, 5) + word) & M32
+    # each of the three terms is a bijective summand: moving r by one moves t by KR
+    A3, _ = oracle.warp_rounds(A, X, region, base, r + 1, r + 2, P=1)
+    t2 = ((y & M32) + (r + 1) * KR + (base & M32) + (base >> 32) * KH) & M32
+    assert int(A3[0, 0]) == (rotl(t2, 5) + word) & M32
 
 
 def test_pick_index_formula():
@@ -178,8 +183,8 @@ def test_chain_multipliers_and_order():
 def test_chain_rotations_on_zero_state():
     """R7 rotate-add amounts S[j]: with a = 0 the chain reduces to
     a[j]' = t_j, t_{j+1} = t_j + rotl(t_j, S[j]); R8 with C = 0 doubles t;
-    R9 gives a[15]' = t_15 ^ (neighbour's final t).  All lanes share x, so all
-    lanes have the same t and a[15]' = t_15 ^ 2*t_16."""
+    R9 gives a[15]' = t_15*KX + (neighbour's final t).  All lanes share x, so all
+    lanes have the same t and a[15]' = t_15*KX + 2*t_16."""
     A, X = _zero_state()
     region = np.zeros(4, dtype=np.uint8)
     A2, _ = oracle.warp_rounds(A, X, region, 0, 0, 1, P=1)
@@ -190,7 +195,7 @@ def test_chain_rotations_on_zero_state():
         expect.append(t)
         t = (t + rotl(t, S_TAB[j])) & M32
     final_t = (t + t) & M32            # R8, N = 0
-    expect[15] ^= final_t              # R9
+    expect[15] = (expect[15] * KX + final_t) & M32      # R9
     assert [int(v) for v in A2[0]] == expect
 
 
@@ -210,11 +215,11 @@ def test_self_modify_shift_examples():
         a15 = (C * ((1 << L_TAB[15]) + 1) + t) & M32
         t = (a15 + rotl(t, S_TAB[15])) & M32
         t1 = (t + (t >> N)) & M32
-        # lane 0 (C = 0) has a[15]' = its own t_15 ^ t1
+        # lane 0 (C = 0) has a[15]' = its own t_15 * KX + t1
         t0 = rotl(y & M32, 5)
         for j in range(15):
             t0 = (t0 + rotl(t0, S_TAB[j])) & M32
-        assert int(A2[0, 15]) == t0 ^ t1
+        assert int(A2[0, 15]) == (t0 * KX + t1) & M32
 
 
 def test_neighbour_exchange_direction():
