@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 METRIC = "checksum rounds/s and checksummed GB/s per B200 (1/2/4/8 GPU); p99 attest time"
 UNIT = "thread-rounds/s"
 
-# Algorithmic 32-bit integer operations per thread-round of SCS-1 (DESIGN.md
+# Algorithmic 32-bit integer operations per thread-round of SCS-2 (DESIGN.md
 # section 7): minimal sm_100 lowering with 3-input LOP3 / IMAD / LEA.HI.
 OPS_PER_ROUND = {1: 59, 4: 62, 8: 67}
 

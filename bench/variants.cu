@@ -1,4 +1,4 @@
-// variants.cu -- development harness: times lowering variants of the SCS-1
+// variants.cu -- development harness: times lowering variants of the SCS-2
 // kernel (sage_kernel.cuh) at full occupancy on one SMEM/GLOBAL workload and
 // checks they all return the same checksum.  Not part of the product path.
 //
@@ -33,7 +33,9 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1), VARA(1, true, false, 0, 1, 1),
+    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1), VARA(1, true, false, 0, 32, 2),
+    VARA(4, true, false, 0, 2, 1), VARA(4, true, false, 0, 2, 2), VARA(4, true, false, 0, 1, 2),
+    VAR(8, false, true, 0, 1), VAR(1, false, true, 0, 16), VAR(4, false, true, 0, 16),
 };
 
 int main(int argc, char** argv) {

@@ -8,7 +8,7 @@
  * of the checksummed region and fold it, the data pointer and the round index
  * into an ordered integer state, and the per-thread states are
  * summed warp -> block -> grid into one value.  The exact
- * arithmetic is SCS-1.
+ * arithmetic is SCS-2.
  *
  * Conventions for every function:
  *   - returns SAGE_OK (0) or a negative SAGE_E* code; never throws/aborts;
@@ -66,7 +66,7 @@ typedef struct {
     uint64_t cycles;      /* max over CTAs of the CTA's clock64 duration */
     uint64_t elapsed_ns;  /* host CLOCK_MONOTONIC from before launch to result on host (t1 - t0) */
     uint64_t device_ns;   /* %globaltimer: last CTA end - first CTA start */
-    uint64_t region_va;   /* device VA the region was read from (the `base` of SCS-1) */
+    uint64_t region_va;   /* device VA the region was read from (the `base` of SCS-2) */
     uint32_t placement;   /* SAGE_SMEM or SAGE_GLOBAL actually used */
     uint32_t blocks;      /* grid actually launched */
     uint32_t threads;     /* block size actually launched */
@@ -88,7 +88,7 @@ typedef struct {
  *              placement unknown, out NULL.  SAGE_ECUDA / SAGE_ENOMEM. */
 int sage_checksum_init(const sage_config* cfg, sage_ctx** out);
 
-/* Synchronous attestation over a DEVICE region (SCS-1 with base = region).
+/* Synchronous attestation over a DEVICE region (SCS-2 with base = region).
  * region_bytes = 4 * P * Nc with Nc a power of two (<= 2^32); region 16-byte
  * aligned (32-byte for P = 8); rounds < 2^32.  Returns when the result is on
  * the host.  SAGE_EINVAL on a violated precondition or NULL pointer;
@@ -135,7 +135,7 @@ int sage_decode_raw(const uint64_t raw[4], sage_result* out);
 
 /* End-to-end form over a HOST region: copies the region host->device into a
  * context-owned device buffer (whose VA is reported in out->region_va and is
- * the SCS-1 base), attests, copies the 32-byte result back.  elapsed_ns covers
+ * the SCS-2 base), attests, copies the 32-byte result back.  elapsed_ns covers
  * the copies.  Pinned host memory gives the fastest copy. */
 int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, size_t region_bytes,
                      uint64_t rounds, sage_result* out);

@@ -110,7 +110,7 @@ int set_device(const sage_ctx* c) {
     return SAGE_OK;
 }
 
-// Check the SCS-1 preconditions on (region, bytes, rounds) for P.
+// Check the SCS-2 preconditions on (region, bytes, rounds) for P.
 int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t rounds) {
     if (c == nullptr) return fail(SAGE_EINVAL, "null context%s");
     if (region == nullptr) return fail(SAGE_EINVAL, "null region%s");

@@ -1,9 +1,9 @@
-// sage_kernel.cuh -- the SCS-1 checksum kernel for sm_100a.
+// sage_kernel.cuh -- the SCS-2 checksum kernel for sm_100a.
 //
 // One launch = one attestation (SAGE section 5.2.2).  Every thread
 // of a full-occupancy grid (2 CTAs x 1024 threads per SM, 32 registers, the
 // B200 analogue of P:612-613) seeds its state from the nonce, runs R rounds of
-// SCS-1 entirely in registers, and the folded states are
+// SCS-2 entirely in registers, and the folded states are
 // reduced warp (shuffle) -> block (shared memory) -> grid (one 64-bit atomic
 // per CTA).
 //
@@ -166,7 +166,7 @@ __device__ __forceinline__ Pick<P> load_shared_addr(uint32_t addr) {
 }
 
 struct KernelArgs {
-    const uint32_t* region;   // device VA of region word 0 (= SCS-1 base)
+    const uint32_t* region;   // device VA of region word 0 (= SCS-2 base)
     uint64_t nonce;
     uint32_t nc_mask;         // Nc - 1
     uint32_t rounds;          // R
@@ -232,7 +232,7 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
     }
 }
 
-// One SCS-1 round (R1-R9) for this thread.
+// One SCS-2 round (R1-R9) for this thread.
 //   P        words per pick (1, 4, 8)
 //   SMEM     region in shared memory (else read from global)
 //   STRADDLE the region's chunk addresses may differ in their high 32 bits
@@ -245,13 +245,11 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 //            rounds of the unrolled trip, or in its first round when EVERY = 0)
 //   COUNT    also count reads per chunk into args.counts (the memory-region
 //            inclusion experiment); not in the timed path
-#ifndef SAGE_DEF
-#define SAGE_DEF 1
-#endif
-constexpr uint32_t kKR = 0x9E3779B1u, kKH = 0x85EBCA77u, kKX = 0xC2B2AE3Du;   // SCS-2 prototype constants
+// SCS-2 R6 / R9 odd multipliers: round index, high DP word, exchanged value.
+constexpr uint32_t kKR = 0x9E3779B1u, kKH = 0x85EBCA77u, kKX = 0xC2B2AE3Du;
 
 template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false>
-__device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
+__device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
                                            const KernelArgs& args, uint64_t policy = 0, bool inject = false) {
     // R1
@@ -269,26 +267,24 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         const uint32_t lo_dp = i * args.four_p + static_cast<uint32_t>(base);
         d = load_shared_addr<P>(addr);
-        t = ((static_cast<uint32_t>(y) ^ r) * args.one + lo_dp) ^ static_cast<uint32_t>(base >> 32);
+        t = static_cast<uint32_t>(y) * args.one + lo_dp + (r * kKR + static_cast<uint32_t>(base >> 32) * kKH);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 1) {
         // shared-window address of the chunk on the FMA pipe; lo32(dp) = addr + (lo32(base) - smem)
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         d = load_shared_addr<P>(addr);
         const uint32_t base_minus_smem = static_cast<uint32_t>(base) - smem_u32(smem_words);   // loop-invariant
-#if SAGE_DEF == 2
+        // lo32(y) + r*KR + lo32(dp) + hi32(dp)*KH with lo32(dp) = addr + base_minus_smem; the bracket is
+        // warp-uniform (uniform datapath)
         t = static_cast<uint32_t>(y) + (r * kKR + base_minus_smem + static_cast<uint32_t>(base >> 32) * kKH) + addr;
-#else
-        t = ((static_cast<uint32_t>(y) ^ r) + addr + base_minus_smem) ^ static_cast<uint32_t>(base >> 32);
-#endif
     } else if constexpr (SMEM && !STRADDLE) {
         const uint32_t v = i * (4u * P);                         // byte offset of the chunk
         d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
-        t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(base) + v) ^ static_cast<uint32_t>(base >> 32);
+        t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
     } else {
         const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);   // R5 (= the global load address)
         if constexpr (SMEM) d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
         else d = load_global<P, LD>(reinterpret_cast<const uint32_t*>(dp), policy);
-        t = ((static_cast<uint32_t>(y) ^ r) + static_cast<uint32_t>(dp)) ^ static_cast<uint32_t>(dp >> 32);
+        t = static_cast<uint32_t>(y) + r * kKR + static_cast<uint32_t>(dp) + static_cast<uint32_t>(dp >> 32) * kKH;
     }
     // R6 (data)
 #pragma unroll
@@ -299,11 +295,6 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
         a[j] = a[j] * args.mul[j] + t;
         t = a[j] + rotl(t, rot_of(j));
     }
-#if SAGE_DEF == 2
-    // R7b: cross-accumulator multiply-adds (FMA pipe), off the t chain
-#pragma unroll
-    for (int j = 0; j < SAGE_R7B; ++j) a[2 * j + 1] = a[2 * j + 1] * args.mul[2 * j] + a[2 * j];
-#endif
     // injected adversary work: dependent ALU ops that leave t unchanged (t ^ 0)
     if (inject) {
         // EXTRA > 0: dependent ALU-pipe ops (t ^ 0); EXTRA < 0: dependent FMA-pipe ops (t * 1)
@@ -315,15 +306,11 @@ __device__ __forceinline__ void scs1_round(uint32_t (&a)[kAccum], uint32_t& xlo,
     }
     // R8
     t = t + (t >> (C & 31u));
-    // R9
-#if SAGE_DEF == 2
+    // R9 (SCS-2: multiply-add exchange)
     a[kAccum - 1] = a[kAccum - 1] * kKX + __shfl_sync(0xFFFFFFFFu, t, src_lane);
-#else
-    a[kAccum - 1] ^= __shfl_sync(0xFFFFFFFFu, t, src_lane);
-#endif
 }
 
-//   ILP      logical SCS-1 warps per hardware warp: 1 = one lane state per
+//   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
 //            CTA x 1024 threads per SM at 64 registers -- the same register file
@@ -364,7 +351,7 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
         }
     }
 
-    // a1: I1-I3.  Hardware warp hw computes the ILP logical SCS-1 warps
+    // a1: I1-I3.  Hardware warp hw computes the ILP logical SCS-2 warps
     // hw*ILP .. hw*ILP+ILP-1 (lane l of each); logical thread g = 32*warp + l.
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t src_lane = (lane + 1u) & 31u;
@@ -400,7 +387,7 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
         for (int u = 0; u < UNROLL; ++u) {
 #pragma unroll
             for (int s = 0; s < ILP; ++s)
-                scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(
+                scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(
                     a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
                     EVERY > 0 ? (u % EVERY == 0) : (u == 0));
         }
@@ -408,7 +395,7 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
     for (; r < rounds; ++r) {
 #pragma unroll
         for (int s = 0; s < ILP; ++s)
-            scs1_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
+            scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
                                                                       args, policy, true);
     }
 

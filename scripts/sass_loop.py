@@ -3,7 +3,7 @@
     python scripts/sass_loop.py <cubin-or-so> [name-filter]
 
 For every kernel: the backward-branch loop with the most SHFL.IDX (one per
-SCS-1 round) is the main loop; prints instructions per round split by pipe
+SCS-2 round) is the main loop; prints instructions per round split by pipe
 (FMA: IMAD*, ALU: LOP3/SHF/IADD3/LEA/..., other)."""
 import re
 import subprocess
