@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 
-PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01",
+PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01", "scs2",
                     "c4_timing.json")
 
 
