@@ -22,20 +22,21 @@
     } while (0)
 
 using Fn = void (*)(const sage::KernelArgs);
-struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; };
+struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; int cluster = 0; };
 
 #define VAR(P, S, ST, XS, U) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U>, P, S, ST}
 #define VARL(P, LD) {"P" #P " global ld" #LD, sage::sage_checksum_kernel<P, false, true, 0, 1, 0, LD>, P, false, true}
 #define VARI(P, U, A, ILP) {"P" #P " smem straddlefalse unroll" #U " addr" #A " ILP" #ILP, \
                            sage::sage_checksum_kernel<P, true, false, 0, U, A, 0, 0, false, 0, ILP>, P, true, false, ILP}
+#define VARC(P, U, CL) {"P" #P " cluster-smem unroll" #U " cluster" #CL, \
+                        sage::sage_checksum_kernel<P, true, false, 0, U, 3, 0, 0, false, 0, 1>, P, true, false, 1, CL}
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1), VARA(1, true, false, 0, 32, 2),
-    VARA(4, true, false, 0, 2, 1), VARA(4, true, false, 0, 2, 2), VARA(4, true, false, 0, 1, 2),
-    VAR(8, false, true, 0, 1), VAR(1, false, true, 0, 16), VAR(4, false, true, 0, 16),
+    VARA(1, true, false, 0, 32, 1), VAR(1, false, true, 0, 16), VARC(1, 1, 8), VARC(1, 8, 8), VARC(1, 16, 8),
+    VARC(1, 8, 4), VARC(1, 8, 2),
 };
 
 int main(int argc, char** argv) {
@@ -68,15 +69,21 @@ int main(int argc, char** argv) {
     for (auto& v : variants) {
         if (only && strstr(v.name, only) == nullptr) continue;
         if (!v.straddle && straddles) continue;
-        if (v.smem && bytes > 65536) continue;
+        size_t dyn = v.smem ? bytes : 0;
+        if (v.cluster) {
+            dyn = bytes / v.cluster;
+            if (dyn > 65536 || dyn < 16) continue;
+        } else if (v.smem && bytes > 65536) continue;
         if (v.smem) CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         sage::KernelArgs a{};
         a.region = reinterpret_cast<const uint32_t*>(d);
         a.nonce = 0x1234;
         a.nc_mask = uint32_t(bytes / (4 * v.P) - 1);
         a.rounds = rounds;
-        a.region_bytes = v.smem ? uint32_t(bytes) : 0;
+        a.region_bytes = uint32_t(dyn);
+        a.slice_shift = 0;
+        while ((size_t(1) << a.slice_shift) < dyn) ++a.slice_shift;
         a.raw = raw;
         sage::fill_tables(a, v.P);
         float best = 1e30f;
@@ -84,7 +91,22 @@ int main(int argc, char** argv) {
         for (int rep = 0; rep < 3; ++rep) {
             CK(cudaMemset(raw, 0, 32));
             CK(cudaEventRecord(e0));
-            v.fn<<<blocks / v.ilp, threads, v.smem ? bytes : 0>>>(a);
+            if (v.cluster) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(blocks);
+                cfg.blockDim = dim3(threads);
+                cfg.dynamicSmemBytes = dyn;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = v.cluster;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                CK(cudaLaunchKernelEx(&cfg, v.fn, a));
+            } else {
+                v.fn<<<blocks / v.ilp, threads, dyn>>>(a);
+            }
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             CK(cudaGetLastError());

@@ -185,6 +185,7 @@ struct KernelArgs {
     uint32_t one;             // 1; multiplier that keeps an add on the FMA pipe (ADDR = 2)
     uint32_t* counts;         // COUNT variant only: per-chunk read counters (inclusion experiment)
     uint64_t* cta_trace;      // optional: per CTA {smid, start ns, end ns, clock64 span} (diagnostics)
+    uint32_t slice_shift;     // ADDR == 3 (cluster-distributed SMEM): log2 of the bytes each CTA holds
 };
 
 // The region staged in shared memory (SMEM placement): namespace-scope so the
@@ -262,7 +263,25 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
     // R4, R5, R6 (first part)
     Pick<P> d;
     uint32_t t;
-    if constexpr (SMEM && !STRADDLE && ADDR == 2) {
+    if constexpr (SMEM && !STRADDLE && ADDR == 3) {
+        // region distributed over the cluster's shared memories: CTA rank k holds
+        // bytes [k << slice_shift, (k+1) << slice_shift); read through DSMEM
+        const uint32_t v = i * args.four_p;
+        const uint32_t owner = v >> args.slice_shift;
+        const uint32_t local = smem_u32(smem_words) + (v & ((1u << args.slice_shift) - 1u));
+        uint32_t raddr;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(local), "r"(owner));
+        if constexpr (P == 1) {
+            asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(d.w[0]) : "r"(raddr) : "memory");
+        } else {
+#pragma unroll
+            for (int h = 0; h < P / 4; ++h)
+                asm volatile("ld.shared::cluster.v4.b32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(d.w[4 * h]), "=r"(d.w[4 * h + 1]), "=r"(d.w[4 * h + 2]), "=r"(d.w[4 * h + 3])
+                             : "r"(raddr + 16 * h) : "memory");
+        }
+        t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 2) {
         // both chunk offsets and the R6 add as IMADs (FMA pipe), sparing the ALU pipe
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         const uint32_t lo_dp = i * args.four_p + static_cast<uint32_t>(base);
@@ -337,14 +356,23 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
             __syncthreads();
             if (threadIdx.x == 0) {
                 mbar_expect_tx(&bar, bytes);
+                uint32_t src0 = 0;                       // ADDR == 3: this CTA's slice of the region
+                if constexpr (ADDR == 3) {
+                    uint32_t rank;
+                    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+                    src0 = rank * bytes;
+                }
                 constexpr uint32_t kChunk = 32768;
                 for (uint32_t off = 0; off < bytes; off += kChunk) {
                     const uint32_t n = (bytes - off < kChunk) ? (bytes - off) : kChunk;
                     bulk_g2s(reinterpret_cast<char*>(smem_words) + off,
-                             reinterpret_cast<const char*>(args.region) + off, n, &bar);
+                             reinterpret_cast<const char*>(args.region) + src0 + off, n, &bar);
                 }
             }
             mbar_wait(&bar, 0);
+            if constexpr (ADDR == 3) {                   // every slice staged before any remote read
+                asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            }
         } else {  // 4- or 8-byte regions: below the bulk-copy granule
             for (uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x) smem_words[k] = args.region[k];
             __syncthreads();
@@ -440,6 +468,9 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
                 tr[3] = static_cast<uint64_t>(c_end - c_start);
             }
         }
+    }
+    if constexpr (ADDR == 3) {                           // keep this CTA's slice alive for remote readers
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 }
 
