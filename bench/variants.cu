@@ -35,8 +35,7 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 32, 1), VAR(1, false, true, 0, 16), VARC(1, 1, 8), VARC(1, 8, 8), VARC(1, 16, 8),
-    VARC(1, 8, 4), VARC(1, 8, 2),
+    VAR(1, false, true, 0, 16), VAR(4, false, true, 0, 16), VAR(8, false, true, 0, 1),
 };
 
 int main(int argc, char** argv) {
@@ -76,6 +75,9 @@ int main(int argc, char** argv) {
         } else if (v.smem && bytes > 65536) continue;
         if (v.smem) CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        if (getenv("CARVEOUT"))
+            CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    atoi(getenv("CARVEOUT"))));
         sage::KernelArgs a{};
         a.region = reinterpret_cast<const uint32_t*>(d);
         a.nonce = 0x1234;

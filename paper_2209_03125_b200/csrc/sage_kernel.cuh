@@ -19,6 +19,13 @@
 // on the ALU pipe, 2 cycles per warp instruction each): R7's a*MUL + t is one
 // IMAD (FMA pipe) and t = a + rotl(t, S) one LEA.HI-class op (ALU pipe),
 // the interleaved shift-and-add pattern of P:651.
+//
+// Template knobs of sage_checksum_kernel.  The product (sage_api.cu) uses
+// XS=0, LD=0, EXTRA=0, COUNT=false (except sage_attest_coverage), ILP=1, and
+// ADDR=1 (P=1,8) / ADDR=2 (P=4) for non-straddling SMEM regions; the other
+// values are lowering alternatives measured by bench/variants.cu and
+// bench/adversary.cu and kept so those measurements stay reproducible
+// (DESIGN.md section 8).
 #pragma once
 #include <stdint.h>
 
@@ -28,7 +35,9 @@ constexpr int kAccum = 16;                                   // K
 constexpr uint64_t kXsMult = 0x2545F4914F6CDD1DULL;          // xorshift64* multiplier
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;           // SplitMix64 increment
 
-// R7 constant tables as compile-time immediates (Q6).
+// R7 constant tables (Q6): rotations are compile-time immediates
+// (one LEA.HI each); the multipliers reach the kernel through KernelArgs::mul
+// (constant bank), see there.
 __host__ __device__ constexpr uint32_t mul_of(int j) {
     constexpr uint32_t e[kAccum] = {5, 11, 3, 17, 9, 23, 7, 13, 29, 2, 19, 6, 15, 27, 4, 21};
     return (1u << e[j]) + 1u;
