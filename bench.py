@@ -148,11 +148,11 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------- oracle arm
-def cpu_oracle_rate(region, base, rounds, warps, P, workers):
-    """Time the oracle (as it stands) on `warps` warps over host cores."""
-    import oracle
+def cpu_oracle_rate(pool, nonce, base, rounds, warps, P):
+    """Time the oracle (as it stands) on `warps` warps over the pool's host cores
+    (workers already started, so process start-up is not timed)."""
     t0 = time.perf_counter()
-    sums = oracle.warp_sums_parallel(0x1234, region, base, rounds, warps, P, workers=workers)
+    sums = pool.warp_sums(nonce, base, rounds, warps, P)
     dt = time.perf_counter() - t0
     return len(warps) * 32 * rounds / dt, dt, sums
 
@@ -172,10 +172,11 @@ def run_reference(args):
     base = 0x7F00_0000_0000
     sample_warps = list(range(4 * cores))
     times = []
-    for k in range(args.warmup + args.steps):
-        rate, dt, _ = cpu_oracle_rate(region, base, R, sample_warps, P, cores)
-        if k >= args.warmup:
-            times.append(dt)
+    with oracle.WarpPool(region, cores) as pool:
+        for k in range(args.warmup + args.steps):
+            rate, dt, _ = cpu_oracle_rate(pool, 0x1234 + k, base, R, sample_warps, P)
+            if k >= args.warmup:
+                times.append(dt)
     tr = len(sample_warps) * 32 * R
     value = tr * len(times) / sum(times)
     sample = "%d warps (%d threads) x %d rounds per step, %s" % (len(sample_warps), 32 * len(sample_warps), R,
@@ -366,7 +367,8 @@ def run_ours(args):
             nw = n // 32
             want = min(nw, 32 * cores)
             sample = sorted(set(int(round(i * (nw - 1) / max(1, want - 1))) for i in range(want)))
-            rate, dt, sums = cpu_oracle_rate(host, region.data_ptr(), R, sample, P, cores)
+            with oracle.WarpPool(host, cores) as pool:
+                rate, dt, sums = cpu_oracle_rate(pool, 0x1234, region.data_ptr(), R, sample, P)
             ok = all(sums[w] == parts[w] for w in sample) and (sum(parts) & (2**64 - 1)) == dbg.checksum
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": "%d warps x %d threads x %d rounds of this workload (%.1f s)"

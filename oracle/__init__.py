@@ -129,12 +129,17 @@ def sha256(r, code):
 
 
 # ---- multi-process driver for large configs (one warp range per task) ----------
+# Workers are spawned (not forked: the caller may hold CUDA / torch threads) and
+# attach to the region through POSIX shared memory instead of pickling it.
 _pool_region = None
+_pool_shm = None
 
 
-def _pool_init(region_bytes):
-    global _pool_region
-    _pool_region = np.frombuffer(region_bytes, dtype=np.uint8)
+def _pool_init(shm_name, nbytes):
+    global _pool_region, _pool_shm
+    from multiprocessing import shared_memory
+    _pool_shm = shared_memory.SharedMemory(name=shm_name)
+    _pool_region = np.ndarray((nbytes,), dtype=np.uint8, buffer=_pool_shm.buf)
 
 
 def _pool_task(args):
@@ -142,13 +147,51 @@ def _pool_task(args):
     return [warp_sum(nonce, _pool_region, base, rounds, w, P) for w in range(w0, w1)]
 
 
+class WarpPool:
+    """A pool of spawned oracle workers sharing one region (POSIX shared memory);
+    reuse it across calls so timings do not include process start-up.
+
+        with WarpPool(region) as pool:
+            sums = pool.warp_sums(nonce, base, rounds, warps, P)
+    """
+
+    def __init__(self, region, workers=None):
+        import multiprocessing as mp
+        from multiprocessing import shared_memory
+        src = np.ascontiguousarray(region).view(np.uint8).reshape(-1) if isinstance(region, np.ndarray) else \
+            np.frombuffer(bytes(region), dtype=np.uint8)
+        build()
+        self.workers = workers or len(os.sched_getaffinity(0))
+        self.shm = shared_memory.SharedMemory(create=True, size=max(1, src.nbytes))
+        np.ndarray((src.nbytes,), dtype=np.uint8, buffer=self.shm.buf)[:] = src
+        self.ex = ProcessPoolExecutor(max_workers=self.workers, mp_context=mp.get_context("spawn"),
+                                      initializer=_pool_init, initargs=(self.shm.name, src.nbytes))
+        list(self.ex.map(_pool_noop, range(self.workers)))          # start every worker now
+
+    def warp_sums(self, nonce, base, rounds, warps, P=1):
+        warps = list(warps)
+        tasks = [(nonce, base, rounds, w, w + 1, P) for w in warps]
+        res = list(self.ex.map(_pool_task, tasks, chunksize=max(1, len(tasks) // (4 * self.workers))))
+        return {w: r[0] for w, r in zip(warps, res)}
+
+    def close(self):
+        self.ex.shutdown()
+        self.shm.close()
+        self.shm.unlink()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def _pool_noop(_):
+    return os.getpid()
+
+
 def warp_sums_parallel(nonce, region, base, rounds, warps, P=1, workers=None):
     """Oracle warp partials for the listed warp indices, spread over host cores.
     The per-warp function is unchanged; this only fans warps out."""
-    warps = list(warps)
-    workers = workers or len(os.sched_getaffinity(0))
-    rb = bytes(np.ascontiguousarray(region).view(np.uint8).reshape(-1)) if isinstance(region, np.ndarray) else bytes(region)
-    tasks = [(nonce, base, rounds, w, w + 1, P) for w in warps]
-    with ProcessPoolExecutor(max_workers=workers, initializer=_pool_init, initargs=(rb,)) as ex:
-        res = list(ex.map(_pool_task, tasks, chunksize=max(1, len(tasks) // (4 * workers))))
-    return {w: r[0] for w, r in zip(warps, res)}
+    with WarpPool(region, workers) as pool:
+        return pool.warp_sums(nonce, base, rounds, warps, P)

@@ -1,0 +1,36 @@
+"""Full-result parity at the bench configuration (configs[1], what bench.py
+times): full occupancy, 8 KiB SMEM region of kernel code, R = 10^5.  Every one
+of the n/32 warp partials and the checksum are recomputed by the C oracle,
+fanned out over the host cores (~1 min on 16 cores)."""
+import os
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle                                                              # noqa: E402
+from paper_2209_03125_b200 import sage                                     # noqa: E402
+from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces   # noqa: E402
+
+pytestmark = pytest.mark.gpu
+M64 = (1 << 64) - 1
+
+
+def test_full_occupancy_full_rounds_every_warp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d = torch.from_numpy(region).to("cuda")
+    R = 100_000
+    nonce = nonces(2)[1]
+    with sage.Context() as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        pw = torch.zeros(n // 32, dtype=torch.int64, device="cuda")
+        res = ctx.attest_debug(nonce, d, R, pw)
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    want = oracle.warp_sums_parallel(nonce, region, d.data_ptr(), R, range(n // 32), 1,
+                                     workers=len(os.sched_getaffinity(0)))
+    bad = [w for w in range(n // 32) if parts[w] != want[w]]
+    assert not bad, bad[:10]
+    assert sum(want.values()) & M64 == res.checksum
