@@ -35,7 +35,7 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VAR(1, false, true, 0, 16), VAR(4, false, true, 0, 16), VAR(8, false, true, 0, 1),
+    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1),
 };
 
 int main(int argc, char** argv) {
