@@ -121,7 +121,7 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -130,6 +130,7 @@ class ClockSampler:
             try:
                 sm.append(float(parts[1]))
                 smax = float(parts[2])
+                power.append(float(parts[3]))
             except ValueError:
                 continue
             for name, val in zip(names, parts[5:9]):
@@ -137,7 +138,8 @@ class ClockSampler:
                     reasons.add(name)
         busy = [v for v in sm if smax and v > 0.5 * smax] or sm
         return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(power) if power else None}
 
 
 def dist_env():
@@ -340,6 +342,8 @@ def run_ours(args):
                               "sigma": statistics.pstdev(att), "threshold_2p5sigma":
                               statistics.mean(att) + 2.5 * statistics.pstdev(att), "n": len(att)},
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
+        if clocks.get("power_w_median"):
+            line["energy_j_per_attestation"] = clocks["power_w_median"] * mean_k
         if placement == "global" and nbytes > (1 << 20):
             achieved = n * R * 32.0 / mean_k / 1e9       # DRAM sectors touched (one 32-B sector per pick)
             ceil = gather_ceiling
