@@ -357,3 +357,22 @@ def test_one_context_shared_by_threads(dev):
         for t in ts:
             t.join()
     assert got == want
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_full_occupancy_wide_picks_sampled(dev, P):
+    """P = 4 (SMEM, 16-B picks) and P = 8 (AUTO -> L1-resident GLOBAL, 32-B picks)
+    at full occupancy, 8 KiB region, 10^4 rounds: Σ-consistency + sampled warps."""
+    region = make_region(8192, prefix=kernel_code_prefix(P, P == 4))
+    d, _keep = to_dev(region, dev)
+    R = 10_000
+    with sage.Context(pick_words=P) as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
+        res = ctx.attest_debug(0xE0 + P, d, R, pw)
+        assert res.placement == (sage.SAGE_SMEM if P == 4 else sage.SAGE_GLOBAL)
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    assert sum(parts) & M64 == res.checksum
+    for w in (0, n // 96, n // 32 - 1):
+        assert parts[w] == oracle.warp_sum(0xE0 + P, region, d.data_ptr(), R, w, P), w
