@@ -1,6 +1,8 @@
 """The C-ABI library loads and exports every symbol include/sage.h declares
 (no compute calls: this runs without a GPU)."""
 import ctypes
+
+import numpy as np
 import os
 import re
 
@@ -62,3 +64,18 @@ def test_no_oracle_in_product_path():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, fn
+
+
+def test_null_context_is_rejected_without_device(lib):
+    """Every entry point checks its context before touching CUDA."""
+    calls = [lambda: sage.attest(None, 0, 0x1000, 1, nbytes=16),
+             lambda: sage.attest_host(None, 0, np.zeros(16, np.uint8), 1),
+             lambda: sage.host_region_va(None, 16),
+             lambda: sage.placement_for(None, 16),
+             lambda: sage.query(None),
+             lambda: sage.kernel_hash(None, b"", None)]
+    for call in calls:
+        with pytest.raises(sage.SageError) as e:
+            call()
+        assert e.value.code == sage.SAGE_EINVAL
+    assert sage.launch_count(None) == 0
