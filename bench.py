@@ -373,10 +373,14 @@ def run_ours(args):
             sample = sorted(set(int(round(i * (nw - 1) / max(1, want - 1))) for i in range(want)))
             with oracle.WarpPool(host, cores) as pool:
                 rate, dt, sums = cpu_oracle_rate(pool, 0x1234, region.data_ptr(), R, sample, P)
+            with oracle.WarpPool(host, 1) as pool1:             # one core, a smaller sample
+                rate1, dt1, sums1 = cpu_oracle_rate(pool1, 0x1234, region.data_ptr(), R, sample[:4], P)
             ok = all(sums[w] == parts[w] for w in sample) and (sum(parts) & (2**64 - 1)) == dbg.checksum
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": "%d warps x %d threads x %d rounds of this workload (%.1f s)"
                                               % (len(sample), 32, R, dt),
+                                    "single_core_value": rate1,
+                                    "single_core_sample": "%d warps (%.1f s)" % (len(sample[:4]), dt1),
                                     "parity_on_sample": ok}
         print(json.dumps(line), flush=True)
     ctx.close()
