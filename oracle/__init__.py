@@ -118,10 +118,10 @@ def attest(nonce, region, base, rounds, blocks, threads, P=1):
 def sha256(r, code):
     """SHA-256(r || code) (SAGE Eq. (9)) from the plain C oracle; r, code bytes-like
     or uint8 ndarrays."""
-    rb = np.frombuffer(bytes(r), dtype=np.uint8) if not isinstance(r, np.ndarray) else r.view(np.uint8).reshape(-1)
-    cb = np.frombuffer(bytes(code), dtype=np.uint8) if not isinstance(code, np.ndarray) else code.view(np.uint8).reshape(-1)
-    rb = np.ascontiguousarray(rb)
-    cb = np.ascontiguousarray(cb)
+    def as_u8(b):
+        return np.ascontiguousarray(b.view(np.uint8).reshape(-1) if isinstance(b, np.ndarray)
+                                    else np.frombuffer(bytes(b), dtype=np.uint8))
+    rb, cb = as_u8(r), as_u8(code)
     out = np.zeros(32, dtype=np.uint8)
     lib().sage_oracle_sha256(rb.ctypes.data_as(ctypes.c_void_p), rb.nbytes, cb.ctypes.data_as(ctypes.c_void_p),
                              cb.nbytes, out.ctypes.data_as(ctypes.c_void_p))

@@ -21,8 +21,9 @@ PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto"}
 
 # every symbol include/sage.h declares
 EXPORTS = ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
-           "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va", "sage_placement_for", "sage_query", "sage_launch_count",
-           "sage_stream", "sage_checksum_destroy", "sage_strerror", "sage_last_error")
+           "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va",
+           "sage_placement_for", "sage_query", "sage_launch_count", "sage_stream", "sage_checksum_destroy",
+           "sage_strerror", "sage_last_error")
 
 
 class SageError(RuntimeError):

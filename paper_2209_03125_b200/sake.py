@@ -98,6 +98,11 @@ def int_bytes(x, group):
     return x.to_bytes((group.p.bit_length() + 7) // 8, "big")
 
 
+def _random_exponent(rng, group):
+    """Secret exponent in [1, p-2] from nbits/8 + 8 random bytes (bias < 2^-64)."""
+    return int.from_bytes(rng(group.nbits // 8 + 8), "big") % (group.p - 2) + 1
+
+
 def challenge_nonce(v2):
     """The checksum challenge derived from v2: its first 8 bytes, little-endian."""
     return int.from_bytes(v2[:8], "little")
@@ -130,7 +135,7 @@ class VerifierSession:
     def start(self):
         if self.state != "init":
             raise AbortState("start twice")
-        self.a = self.fixed_secret or int.from_bytes(self.rng(self.group.nbits // 8 + 8), "big") % (self.group.p - 2) + 1
+        self.a = self.fixed_secret or _random_exponent(self.rng, self.group)
         v0 = int_bytes(pow(self.group.g, self.a, self.group.p), self.group)
         v1 = H(v0)
         v2 = H(v1)
@@ -204,7 +209,7 @@ class DeviceSession:
         self.v2 = v2
         self.state = "sent_w2"
         tag = mac(c_bytes(c), w2)
-        self.b = self.fixed_secret or int.from_bytes(self.rng(self.group.nbits // 8 + 8), "big") % (self.group.p - 2) + 1
+        self.b = self.fixed_secret or _random_exponent(self.rng, self.group)
         return w2, tag
 
     def on_v1(self, v1):

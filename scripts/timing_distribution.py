@@ -16,7 +16,6 @@ not import the oracle).
 """
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -77,6 +76,12 @@ def run(rounds_list, counts, samples_per_r, out):
             model = verifier.calibrate(el[:half], min_runs=min(30, half))
             fp = sum(1 for x in el[half:] if x > model.threshold) / max(1, len(el) - half)
             model_all = verifier.calibrate(el, min_runs=min(30, len(el)))
+            quantile_fp = {}
+            for q in (0.95, 0.99):                               # SPEC S:311 empirical-quantile rule
+                qm = verifier.calibrate_quantile(el[:half], q=q, min_runs=min(30, half))
+                quantile_fp["q%.2f" % q] = {"threshold": qm.threshold,
+                                            "false_positive_rate_second_half":
+                                                sum(1 for x in el[half:] if x > qm.threshold) / max(1, len(el) - half)}
             skew, kurt = moments(el)
             entry = {"rounds": R, "n_attest": len(el), "wall_s": time.time() - t_start,
                      "elapsed_s": {"p50": verifier.percentile(el, 50), "p99": verifier.percentile(el, 99),
@@ -89,10 +94,12 @@ def run(rounds_list, counts, samples_per_r, out):
                      "calibrated_on_first_half": {"t_avg": model.t_avg, "sigma": model.sigma,
                                                   "threshold": model.threshold},
                      "false_positive_rate_second_half": fp, "normal_tail_2p5": verifier.normal_tail(2.5),
+                     "quantile_rule": quantile_fp,
                      "thread_rounds_per_s_p50": n * R / verifier.percentile(el, 50),
-                     "sum_of_partials_ok": sum_ok, "samples": samples}
+                     "sum_of_partials_ok": sum_ok, "samples": samples,
+                     "elapsed_ns_all": [int(round(x * 1e9)) for x in el]}
             result["per_R"].append(entry)
-            print(json.dumps({k: v for k, v in entry.items() if k != "samples"}), flush=True)
+            print(json.dumps({k: v for k, v in entry.items() if k not in ("samples", "elapsed_ns_all")}), flush=True)
     with open(out, "w") as f:
         json.dump(result, f, indent=1)
 

@@ -36,7 +36,8 @@ def test_arch_is_sm100a(sass):
 
 def test_smem_kernels_use_tma_bulk_copy(sass):
     funcs = _functions(sass)
-    smem = [n for n in funcs if n.startswith("_ZN4sage20sage_checksum_kernelILi") and "ELb1E" in n.split("ILi", 1)[1][:6]]
+    prefix = "_ZN4sage20sage_checksum_kernelILi"
+    smem = [n for n in funcs if n.startswith(prefix) and "ELb1E" in n[len(prefix):][:6]]   # <P, SMEM=true, ...>
     assert smem, "no SMEM checksum kernels found"
     for n in smem:
         body = funcs[n]
