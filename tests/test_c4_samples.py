@@ -11,13 +11,15 @@ import pytest
 
 import oracle
 
-PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01", "scs2",
-                    "c4_timing.json")
+DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01", "scs2")
+PATHS = [os.path.join(DIR, f) for f in ("c4_timing.json", "c4_timing_full.json")]
 
 
-@pytest.mark.skipif(not os.path.exists(PATH), reason="no config-4 capture committed")
-def test_c4_sampled_warps_match_oracle():
-    with open(PATH) as f:
+@pytest.mark.parametrize("path", PATHS)
+def test_c4_sampled_warps_match_oracle(path):
+    if not os.path.exists(path):
+        pytest.skip("no config-4 capture committed")
+    with open(path) as f:
         d = json.load(f)
     region = np.frombuffer(bytes.fromhex(d["region_hex"]), dtype=np.uint8)
     checked = 0
