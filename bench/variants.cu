@@ -22,7 +22,7 @@
     } while (0)
 
 using Fn = void (*)(const sage::KernelArgs);
-struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; int cluster = 0; };
+struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; int cluster = 0; int stage = 0; };
 
 #define VAR(P, S, ST, XS, U) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U>, P, S, ST}
@@ -31,11 +31,23 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                            sage::sage_checksum_kernel<P, true, false, 0, U, A, 0, 0, false, 0, ILP>, P, true, false, ILP}
 #define VARC(P, U, CL) {"P" #P " cluster-smem unroll" #U " cluster" #CL, \
                         sage::sage_checksum_kernel<P, true, false, 0, U, 3, 0, 0, false, 0, 1>, P, true, false, 1, CL}
+#define VARH(P, U, ILP, ST) {"P" #P " hybrid unroll" #U " ILP" #ILP " stage" #ST, \
+                           sage::sage_checksum_kernel<P, true, false, 0, U, 7, 0, 0, false, 0, ILP>, P, true, false, ILP, 0, ST}
+#define VARG(P, U, ILP) {"P" #P " global unroll" #U " ILP" #ILP, \
+                           sage::sage_checksum_kernel<P, false, false, 0, U, 0, 0, 0, false, 0, ILP>, P, false, false, ILP}
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 0, 16, 1),
+    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 16, 32, 4),
+    VARA(1, true, true, 0, 16, 0), VARA(1, true, true, 16, 16, 0),
+    VARA(4, true, false, 0, 2, 2), VARA(4, true, false, 16, 2, 2), VARA(4, true, false, 16, 2, 4),
+    VARA(4, true, false, 16, 4, 4), VARA(4, true, false, 16, 8, 4),
+    VARA(8, true, false, 0, 1, 1), VARA(8, true, false, 16, 1, 1),
+    VARA(1, false, true, 0, 16, 0), VARA(1, false, true, 16, 16, 0),
+    VARA(4, false, true, 0, 16, 0), VARA(4, false, true, 16, 16, 0),
+    VARA(8, false, true, 0, 1, 0), VARA(8, false, true, 16, 1, 0),
+    VARH(1, 1, 2, 163840), VARH(1, 1, 2, 180224), VARH(1, 1, 2, 196608), VARH(1, 1, 2, 212992),
 };
 
 int main(int argc, char** argv) {
@@ -69,7 +81,10 @@ int main(int argc, char** argv) {
         if (only && strstr(v.name, only) == nullptr) continue;
         if (!v.straddle && straddles) continue;
         size_t dyn = v.smem ? bytes : 0;
-        if (v.cluster) {
+        if (v.stage) {
+            if ((size_t)v.stage >= bytes) continue;
+            dyn = v.stage;
+        } else if (v.cluster) {
             dyn = bytes / v.cluster;
             if (dyn > 65536 || dyn < 16) continue;
         } else if (v.smem && bytes > 65536) continue;

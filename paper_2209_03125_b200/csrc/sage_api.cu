@@ -55,17 +55,27 @@ using KernelFn = void (*)(const sage::KernelArgs);
 template <int P> struct Unroll;
 template <> struct Unroll<1> { static constexpr int smem = 32, smem_straddle = 16, global = 16; };
 template <> struct Unroll<4> { static constexpr int smem = 2, smem_straddle = 2, global = 16; };
+// Lowering choices per P (bench/variants.cu; profiles/r01/variants/lowering_scs2_*.jsonl):
+//   Addr: pick addressing of non-straddling SMEM regions (ADDR 4 = R6 bracket folded into
+//         the chunk-offset IMAD, ADDR 2 = both offsets as IMADs);
+//   XsSmem / XsGlobal: 16 = x*M64 as one wide multiply + two chained IMADs.
+// P=1 SMEM: ADDR 4 + XS 16 55.33 ms vs 55.93 (ADDR 1, XS 0) at c2a; P=4 SMEM keeps ADDR 2,
+// XS 0 (62.1 vs 62.7 ms); GLOBAL: XS 16 is 0.4-1% faster for every P.
 template <int P> struct Addr { static constexpr int mode = 1; };
+template <> struct Addr<1> { static constexpr int mode = 4; };
 template <> struct Addr<4> { static constexpr int mode = 2; };   // measured: 64.52 vs 65.43 ms at 8 KiB
+template <int P> struct XsSmem { static constexpr int xs = 0; };
+template <> struct XsSmem<1> { static constexpr int xs = 16; };
+constexpr int kXsGlobal = 16;
 template <> struct Unroll<8> { static constexpr int smem = 1, smem_straddle = 1, global = 1; };
 
 template <int P>
 KernelFn kernel_for_p(bool smem, bool straddle) {
     if (smem) {
         return straddle ? sage::sage_checksum_kernel<P, true, true, 0, Unroll<P>::smem_straddle, 0, 0>
-                        : sage::sage_checksum_kernel<P, true, false, 0, Unroll<P>::smem, Addr<P>::mode, 0>;
+                        : sage::sage_checksum_kernel<P, true, false, XsSmem<P>::xs, Unroll<P>::smem, Addr<P>::mode, 0>;
     }
-    return sage::sage_checksum_kernel<P, false, true, 0, Unroll<P>::global, 0, 0>;
+    return sage::sage_checksum_kernel<P, false, true, kXsGlobal, Unroll<P>::global, 0, 0>;
 }
 
 KernelFn kernel_for(uint32_t P, bool smem, bool straddle) {

@@ -21,9 +21,10 @@
 // the interleaved shift-and-add pattern of P:651.
 //
 // Template knobs of sage_checksum_kernel.  The product (sage_api.cu) uses
-// XS=0, LD=0, EXTRA=0, COUNT=false (except sage_attest_coverage), ILP=1, and
-// ADDR=1 (P=1,8) / ADDR=2 (P=4) for non-straddling SMEM regions; the other
-// values are lowering alternatives measured by bench/variants.cu and
+// LD=0, EXTRA=0, COUNT=false (except sage_attest_coverage), ILP=1;
+// XS=16 for P=1 SMEM and for every GLOBAL kernel (XS=0 otherwise); and
+// ADDR=4 (P=1) / ADDR=2 (P=4) / ADDR=1 (P=8) for non-straddling SMEM regions;
+// the other values are lowering alternatives measured by bench/variants.cu and
 // bench/adversary.cu and kept so those measurements stay reproducible
 // (DESIGN.md section 8).
 #pragma once
@@ -264,7 +265,22 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                                            const KernelArgs& args, uint64_t policy = 0, bool inject = false) {
     // R1
     xorshift_split<XS>(xlo, xhi, args);
-    const uint64_t y = ((static_cast<uint64_t>(xhi) << 32) | xlo) * kXsMult;
+    uint64_t y;
+    if constexpr (XS & 16) {
+        // y = x * M64 (mod 2^64) as one wide multiply and two chained multiply-adds
+        // (3 FMA-pipe ops; ptxas' own lowering uses 4 to shorten the latency)
+        uint32_t ylo, yhi;
+        asm("{\n\t.reg .u64 w;\n\t"
+            "mul.wide.u32 w, %2, %4;\n\t"
+            "mov.b64 {%0, %1}, w;\n\t"
+            "mad.lo.u32 %1, %2, %5, %1;\n\t"
+            "mad.lo.u32 %1, %3, %4, %1;\n\t}"
+            : "=&r"(ylo), "=&r"(yhi)
+            : "r"(xlo), "r"(xhi), "n"(static_cast<uint32_t>(kXsMult)), "n"(static_cast<uint32_t>(kXsMult >> 32)));
+        y = (static_cast<uint64_t>(yhi) << 32) | ylo;
+    } else {
+        y = ((static_cast<uint64_t>(xhi) << 32) | xlo) * kXsMult;
+    }
     // R2, R3
     const uint32_t C = a[kAccum - 1];
     const uint32_t i = (static_cast<uint32_t>(y >> 32) ^ C) & nc_mask;
@@ -290,6 +306,57 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                              : "r"(raddr + 16 * h) : "memory");
         }
         t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 4) {
+        // as ADDR == 2, with the whole warp-uniform bracket folded into the chunk-offset IMAD
+        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
+        const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        d = load_shared_addr<P>(addr);
+        t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 7) {
+        // hybrid placement: the first region_bytes of the region are staged in shared
+        // memory, the rest is read from global (L1/L2); each lane loads from whichever
+        // holds its chunk (predicated LDS / LDG, so a lane touches one of the two)
+        const uint32_t v = i * args.four_p;
+        const uint32_t saddr = v + smem_u32(smem_words);
+        const uint64_t gaddr = base + v;
+        const uint32_t staged = args.region_bytes;
+        if constexpr (P == 1) {
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %1, %2;\n\t"
+                         "@p ld.shared.b32 %0, [%3];\n\t"
+                         "@!p ld.global.nc.b32 %0, [%4];\n\t}"
+                         : "=r"(d.w[0]) : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
+        } else if constexpr (P == 4) {
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %4, %5;\n\t"
+                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%6];\n\t"
+                         "@!p ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%7];\n\t}"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3])
+                         : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
+        } else {
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %8, %9;\n\t"
+                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%10];\n\t"
+                         "@p ld.shared.v4.b32 {%4,%5,%6,%7}, [%10+16];\n\t"
+                         "@!p ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%11];\n\t}"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7])
+                         : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
+        }
+        t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 5) {
+        // lo32(y) + 4P*i in one IMAD, then the warp-uniform bracket
+        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
+        const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        d = load_shared_addr<P>(addr);
+        t = (i * args.four_p + static_cast<uint32_t>(y)) + ur;
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 6) {
+        // lo32(y)*1 + addr (FMA pipe), then the warp-uniform bracket (which absorbs -smem)
+        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
+        const uint32_t ur = r * kKR + (static_cast<uint32_t>(base) - smem_u32(smem_words)) +
+                            static_cast<uint32_t>(base >> 32) * kKH;
+        d = load_shared_addr<P>(addr);
+        t = (static_cast<uint32_t>(y) * args.one + addr) + ur;
     } else if constexpr (SMEM && !STRADDLE && ADDR == 2) {
         // both chunk offsets and the R6 add as IMADs (FMA pipe), sparing the ALU pipe
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
