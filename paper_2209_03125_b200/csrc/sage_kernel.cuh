@@ -259,7 +259,8 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 // SCS-2 R6 / R9 odd multipliers: round index, high DP word, exchanged value.
 constexpr uint32_t kKR = 0x9E3779B1u, kKH = 0x85EBCA77u, kKX = 0xC2B2AE3Du;
 
-template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false>
+template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false,
+          int PROBE = 0>
 __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
                                            const KernelArgs& args, uint64_t policy = 0, bool inject = false) {
@@ -310,7 +311,8 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         // as ADDR == 2, with the whole warp-uniform bracket folded into the chunk-offset IMAD
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
-        d = load_shared_addr<P>(addr);
+        if constexpr (PROBE & 1) d.w[0] = addr;                 // probe only: no shared-memory load
+        else d = load_shared_addr<P>(addr);
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 7) {
         // hybrid placement: the first region_bytes of the region are staged in shared
@@ -402,16 +404,21 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
     // R8
     t = t + (t >> (C & 31u));
     // R9 (SCS-2: multiply-add exchange)
-    a[kAccum - 1] = a[kAccum - 1] * kKX + __shfl_sync(0xFFFFFFFFu, t, src_lane);
+    if constexpr (PROBE & 2) a[kAccum - 1] = a[kAccum - 1] * kKX + t;    // probe only: no exchange
+    else a[kAccum - 1] = a[kAccum - 1] * kKX + __shfl_sync(0xFFFFFFFFu, t, src_lane);
 }
 
+//   PROBE    measurement-only instruction-mix probes (never in the product; the
+//            checksum is then not SCS-2): bit 0 replaces the pick's shared-memory
+//            load by its address (ADDR == 4 only), bit 1 the neighbour exchange by
+//            the lane's own t, so the loop keeps only its integer arithmetic
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
 //            CTA x 1024 threads per SM at 64 registers -- the same register file
 //            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
-          bool COUNT = false, int EVERY = 0, int ILP = 1>
+          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0>
 __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
         for (int u = 0; u < UNROLL; ++u) {
 #pragma unroll
             for (int s = 0; s < ILP; ++s)
-                scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(
+                scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(
                     a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
                     EVERY > 0 ? (u % EVERY == 0) : (u == 0));
         }
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
     for (; r < rounds; ++r) {
 #pragma unroll
         for (int s = 0; s < ILP; ++s)
-            scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
+            scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
                                                                       args, policy, true);
     }
 
