@@ -73,3 +73,22 @@ def test_registers_allow_two_ctas_of_1024(res_usage):
         if n.endswith("ILi2EEEvNS_10KernelArgsE"):       # ILP=2 variants (not instantiated in the product)
             continue
         assert r <= 32, (n, r)
+
+
+def test_c2a_kernel_op_mix():
+    """The c2a product kernel (P=1, SMEM, non-straddling, XS=16, ADDR=4): per
+    unrolled round at most 30 ALU-pipe and 26 FMA-pipe instructions (one of them
+    the IMAD.WIDE of x*M64), one LDS and one SHFL.IDX -- the minimum ALU count
+    for SCS-2's shift/xor/rotate steps (DESIGN.md sections 7-8)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import sass_loop
+    build.build()
+    res = sass_loop.analyse(build.CUBIN, "ILi1ELb1ELb0ELi16ELi32ELi4E")
+    assert len(res) == 1, sorted(res)
+    (d,) = res.values()
+    assert d["rounds"] == 32
+    assert d["alu"] <= 30.1, d
+    assert d["fma"] <= 26.1 and d["wide"] == 1.0, d
+    assert d["hist"].get("LDS", 0) == 32 and d["hist"].get("SHFL.IDX", 0) == 32, d
