@@ -34,17 +34,25 @@
     } while (0)
 
 using Fn = void (*)(const sage::KernelArgs);
-struct K { const char* name; Fn fn; int extra; int every; };
+struct K { const char* name; Fn fn; int extra; int every; int ilp = 1; };
 
-// <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA, COUNT, EVERY>; the honest
-// kernel is the product's c2a kernel (UNROLL 32, ADDR 1)
+// <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA, COUNT, EVERY, ILP, PROBE, PAD>; the
+// honest kernel is the product's c2a kernel (XS 16, UNROLL 16, ADDR 4, ILP 2, PAD 10)
 static K kernels[] = {
-    {"honest", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 0>, 0, 0},
-    {"+1 instr / round", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 1, false, 1>, 1, 1},
-    {"+1 instr / 8 rounds", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 1, false, 8>, 1, 8},
-    {"+1 instr / 32 rounds", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, 1, false, 32>, 1, 32},
-    {"+1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, -1, false, 1>, -1, 1},
-    {"+2 IMAD / round", sage::sage_checksum_kernel<1, true, false, 0, 32, 1, 0, -2, false, 1>, -2, 1},
+    {"honest", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10>, 0, 0, 2},
+    {"+1 instr / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 1, 2, 0, 10>, 1, 1, 2},
+    {"+1 instr / 8 rounds", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 8, 2, 0, 10>, 1, 8, 2},
+    {"+1 instr / 16 rounds", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 16, 2, 0, 10>, 1, 16, 2},
+    {"+1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -1, false, 1, 2, 0, 10>, -1, 1, 2},
+    {"+2 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -2, false, 1, 2, 0, 10>, -2, 1, 2},
+    // other implementations of the same function an adversary could switch to:
+    // the ILP 1 kernel (2 CTAs x 1024 threads per SM, 32 registers; the previous
+    // product) and the ILP 2 kernel without the register reservation (56 registers)
+    {"ILP1 (2 CTAs/SM)", sage::sage_checksum_kernel<1, true, false, 16, 32, 4, 0, 0>, 0, 0, 1},
+    {"ILP1 +1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 32, 4, 0, -1, false, 1>, -1, 1, 1},
+    {"ILP2 unpadded", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2>, 0, 0, 2},
+    {"ILP2 unpadded +1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -1, false, 1, 2>, -1, 1, 2},
+    {"ILP2 unpadded +1 instr / 16", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 16, 2>, 1, 16, 2},
 };
 
 static uint64_t now_ns() {
@@ -95,7 +103,7 @@ int main(int argc, char** argv) {
         for (int j = 0; j < nk; ++j) {
             const uint64_t t0 = now_ns();
             CK(cudaMemsetAsync(raw, 0, 32, s));
-            kernels[j].fn<<<blocks, threads, bytes, s>>>(args[j]);
+            kernels[j].fn<<<blocks / kernels[j].ilp, threads, bytes, s>>>(args[j]);
             CK(cudaMemcpyAsync(hraw, raw, 32, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             const uint64_t t1 = now_ns();
@@ -127,8 +135,8 @@ int main(int argc, char** argv) {
         fflush(stdout);
     }
     // verdicts: adversary vs the honest kernel with the same unroll
-    const int pairs[][2] = {{0, 1}, {0, 2}, {0, 3}, {0, 4}, {0, 5}};
-    for (auto& p : pairs) {
+    for (int jj = 1; jj < nk; ++jj) {
+        const int p[2] = {0, jj};
         const Stat& hs = st[p[0]];
         const Stat& as = st[p[1]];
         // calibrate on the first half of the honest runs, evaluate on the second half

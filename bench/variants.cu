@@ -22,7 +22,7 @@
     } while (0)
 
 using Fn = void (*)(const sage::KernelArgs);
-struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; int cluster = 0; int stage = 0; int probe = 0; };
+struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1; int cluster = 0; int stage = 0; int probe = 0; int threads = 1024; };
 
 #define VAR(P, S, ST, XS, U) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U>, P, S, ST}
@@ -39,11 +39,14 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                            sage::sage_checksum_kernel<P, true, false, XS, U, A, 0, 0, false, 0, ILP>, P, true, false, ILP}
 #define VARP(PR) {"P1 smem xs16 unroll32 addr4 PROBE" #PR, \
                   sage::sage_checksum_kernel<1, true, false, 16, 32, 4, 0, 0, false, 0, 1, PR>, 1, true, false, 1, 0, 0, PR}
+#define VARQ(U, ILP, PAD, T) {"P1 smem xs16 unroll" #U " addr4 ILP" #ILP " PAD" #PAD " T" #T, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, 0, false, 0, ILP, 0, PAD>, 1, true, false, ILP, 0, 0, 0, T}
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 0, 32, 1), VARA(1, true, false, 16, 32, 4), VARP(1), VARP(2), VARP(3),
+    VARA(1, true, false, 16, 32, 4), VARQ(16, 2, 0, 1024), VARQ(16, 2, 8, 1024), VARQ(16, 2, 10, 1024),
+    VARQ(8, 4, 0, 512), VARQ(4, 4, 0, 512), VARQ(8, 4, 0, 256), VARQ(16, 2, 0, 512),
 };
 
 int main(int argc, char** argv) {
@@ -118,7 +121,7 @@ int main(int argc, char** argv) {
                 cfg.numAttrs = 1;
                 CK(cudaLaunchKernelEx(&cfg, v.fn, a));
             } else {
-                v.fn<<<blocks / v.ilp, threads, dyn>>>(a);
+                v.fn<<<blocks * threads / (v.ilp * v.threads), v.threads, dyn>>>(a);
             }
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));

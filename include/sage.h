@@ -71,6 +71,9 @@ typedef struct {
     uint32_t blocks;      /* grid actually launched */
     uint32_t threads;     /* block size actually launched */
     uint32_t pick_words;  /* P actually used */
+    uint32_t ilp;         /* logical lane states per hardware thread (1 or 2): the launch was
+                             blocks/ilp CTAs of `threads`, covering the same blocks*threads
+                             logical threads (the c2a kernel uses 2) */
 } sage_result;
 
 typedef struct {
@@ -81,6 +84,7 @@ typedef struct {
     uint32_t ctas_per_sm_global;
     uint32_t regs_per_thread;  /* of the P-specific SMEM kernel */
     uint64_t smem_region_max;  /* largest region (bytes) SAGE_AUTO stages into SMEM */
+    uint32_t ilp_smem;         /* lane states per thread of that SMEM kernel (1 or 2) */
 } sage_info;
 
 /* Create a context on cfg->device.  cfg may be NULL (all defaults).

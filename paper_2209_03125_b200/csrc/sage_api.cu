@@ -69,8 +69,26 @@ template <> struct XsSmem<1> { static constexpr int xs = 16; };
 constexpr int kXsGlobal = 16;
 template <> struct Unroll<8> { static constexpr int smem = 1, smem_straddle = 1, global = 1; };
 
+// c2a geometry (P = 1, SMEM, non-straddling, 1024-thread blocks, even block count):
+// two logical lane states per hardware thread (ILP 2), one CTA of 1024 threads per SM,
+// with PAD registers reserved so the CTA allocates the whole 64 K register file
+// (64 registers x 1024 threads) and no other kernel can become resident beside it
+// (P:343-344).  Measured 54.87 vs 55.33 ms per c2a attestation, and it is the
+// fastest implementation of SCS-2 found: an adversary that
+// switched to it would otherwise gain ~0.8% of slack for injected work (section 11).
+constexpr int kIlpSmem = 2, kIlpPad = 10, kIlpUnroll = 16;
+
+uint32_t ilp_for(uint32_t P, bool smem, bool straddle, uint32_t blocks, uint32_t threads) {
+    return (P == 1 && smem && !straddle && threads == 1024 && blocks % kIlpSmem == 0) ? kIlpSmem : 1;
+}
+
 template <int P>
-KernelFn kernel_for_p(bool smem, bool straddle) {
+KernelFn kernel_for_p(bool smem, bool straddle, uint32_t ilp) {
+    if constexpr (P == 1) {
+        if (ilp == kIlpSmem && smem && !straddle)
+            return sage::sage_checksum_kernel<1, true, false, XsSmem<1>::xs, kIlpUnroll, Addr<1>::mode, 0, 0, false, 0,
+                                              kIlpSmem, 0, kIlpPad>;
+    }
     if (smem) {
         return straddle ? sage::sage_checksum_kernel<P, true, true, 0, Unroll<P>::smem_straddle, 0, 0>
                         : sage::sage_checksum_kernel<P, true, false, XsSmem<P>::xs, Unroll<P>::smem, Addr<P>::mode, 0>;
@@ -78,11 +96,11 @@ KernelFn kernel_for_p(bool smem, bool straddle) {
     return sage::sage_checksum_kernel<P, false, true, kXsGlobal, Unroll<P>::global, 0, 0>;
 }
 
-KernelFn kernel_for(uint32_t P, bool smem, bool straddle) {
+KernelFn kernel_for(uint32_t P, bool smem, bool straddle, uint32_t ilp = 1) {
     switch (P) {
-        case 1: return kernel_for_p<1>(smem, straddle);
-        case 4: return kernel_for_p<4>(smem, straddle);
-        case 8: return kernel_for_p<8>(smem, straddle);
+        case 1: return kernel_for_p<1>(smem, straddle, ilp);
+        case 4: return kernel_for_p<4>(smem, straddle, ilp);
+        case 8: return kernel_for_p<8>(smem, straddle, ilp);
         default: return nullptr;
     }
 }
@@ -147,14 +165,15 @@ uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
 }
 
 int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
-           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr) {
+           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
     const uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
     if (placement == SAGE_SMEM && bytes > kSmemRegionMax)
         return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s", "64 KiB");
     const bool smem = placement == SAGE_SMEM;
     const uint64_t lo = reinterpret_cast<uint64_t>(region);
     const bool straddle = (lo >> 32) != ((lo + bytes - 1) >> 32);
-    KernelFn fn = counts ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle);
+    const uint32_t ilp = counts ? 1 : ilp_for(c->pick_words, smem, straddle, c->blocks, c->threads);
+    KernelFn fn = counts ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle, ilp);
     const size_t dyn = smem ? bytes : 0;
     if (smem) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
@@ -168,16 +187,18 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     args.per_warp = per_warp;
     args.counts = counts;
     sage::fill_tables(args, c->pick_words);
-    fn<<<c->blocks, c->threads, dyn, c->stream>>>(args);
+    fn<<<c->blocks / ilp, c->threads, dyn, c->stream>>>(args);
     CUDA_TRY(cudaGetLastError());
     c->launches++;
     if (placement_used) *placement_used = placement;
+    if (ilp_used) *ilp_used = ilp;
     return SAGE_OK;
 }
 
 void fill_result(const sage_ctx* c, const uint64_t raw[4], uint64_t t0, uint64_t t1, uint64_t va, uint32_t placement,
-                 sage_result* out) {
+                 uint32_t ilp, sage_result* out) {
     sage_decode_raw(raw, out);
+    out->ilp = ilp;
     out->elapsed_ns = t1 - t0;
     out->region_va = va;
     out->placement = placement;
@@ -194,13 +215,13 @@ int attest_device(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes,
     const uint64_t t0 = now_ns();
     if (host_src) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(region), host_src, bytes, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_raw, 0, 4 * sizeof(uint64_t), c->stream));
-    uint32_t placement = 0;
-    rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts);
+    uint32_t placement = 0, ilp = 1;
+    rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts, &ilp);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->h_raw, c->d_raw, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     const uint64_t t1 = now_ns();
-    fill_result(c, c->h_raw, t0, t1, reinterpret_cast<uint64_t>(region), placement, out);
+    fill_result(c, c->h_raw, t0, t1, reinterpret_cast<uint64_t>(region), placement, ilp, out);
     return SAGE_OK;
 }
 
@@ -387,7 +408,9 @@ int sage_query(sage_ctx* ctx, sage_info* out) {
     info.pick_words = ctx->pick_words;
     info.placement = ctx->placement;
     info.smem_region_max = kSmemRegionMax;
-    KernelFn fs = kernel_for(ctx->pick_words, true, false), fg = kernel_for(ctx->pick_words, false, true);
+    const uint32_t ilp = ilp_for(ctx->pick_words, true, false, ctx->blocks, ctx->threads);
+    info.ilp_smem = ilp;
+    KernelFn fs = kernel_for(ctx->pick_words, true, false, ilp), fg = kernel_for(ctx->pick_words, false, true);
     CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fs), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemRegionMax)));
     int occ = 0;

@@ -412,14 +412,16 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //            checksum is then not SCS-2): bit 0 replaces the pick's shared-memory
 //            load by its address (ADDR == 4 only), bit 1 the neighbour exchange by
 //            the lane's own t, so the loop keeps only its integer arithmetic
+//   PAD      registers reserved (kept live across the round loop, unused) so that
+//            an ILP > 1 kernel allocates the whole register file
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
 //            CTA x 1024 threads per SM at 64 registers -- the same register file
 //            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
-          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0>
-__global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
+          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0>
+__global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint64_t t_start_ns;
@@ -484,6 +486,17 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
         xhi[s] = static_cast<uint32_t>(x >> 32);
     }
 
+    // PAD: register reservation -- PAD per-lane values from %clock (not recomputable)
+    // before the round loop and consumed after it, so they stay in registers for
+    // the whole attestation and the CTA's register allocation grows by PAD
+    uint32_t pad[PAD > 0 ? PAD : 1];
+    if constexpr (PAD > 0) {
+#pragma unroll
+        for (int k = 0; k < PAD; ++k)          // per-lane values, so they occupy vector registers
+            asm volatile("{\n\t.reg .b32 c;\n\tmov.u32 c, %%clock;\n\tmov.u32 %0, %%laneid;\n\t"
+                         "add.u32 %0, %0, c;\n\t}" : "=r"(pad[k]));
+    }
+
     const uint64_t base = reinterpret_cast<uint64_t>(args.region);
     const uint32_t nc_mask = args.nc_mask;
     const uint32_t rounds = args.rounds;
@@ -508,6 +521,13 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
         for (int s = 0; s < ILP; ++s)
             scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
                                                                       args, policy, true);
+    }
+
+    if constexpr (PAD > 0) {
+#pragma unroll
+        for (int k = 0; k < PAD; ++k)          // xlo ^= pad & 0 (args.zero): result-neutral
+            asm volatile("{\n\t.reg .b32 q;\n\tand.b32 q, %1, %2;\n\txor.b32 %0, %0, q;\n\t}"
+                         : "+r"(xlo[0]) : "r"(pad[k]), "r"(args.zero));
     }
 
     // a11: F1-F2, a12: warp -> block -> grid

@@ -40,7 +40,8 @@ class sage_config(ctypes.Structure):
 class sage_result(ctypes.Structure):
     _fields_ = [("checksum", ctypes.c_uint64), ("cycles", ctypes.c_uint64), ("elapsed_ns", ctypes.c_uint64),
                 ("device_ns", ctypes.c_uint64), ("region_va", ctypes.c_uint64), ("placement", ctypes.c_uint32),
-                ("blocks", ctypes.c_uint32), ("threads", ctypes.c_uint32), ("pick_words", ctypes.c_uint32)]
+                ("blocks", ctypes.c_uint32), ("threads", ctypes.c_uint32), ("pick_words", ctypes.c_uint32),
+                ("ilp", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -50,7 +51,8 @@ class sage_info(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("sm_count", ctypes.c_uint32), ("blocks", ctypes.c_uint32),
                 ("threads", ctypes.c_uint32), ("pick_words", ctypes.c_uint32), ("placement", ctypes.c_uint32),
                 ("ctas_per_sm_smem", ctypes.c_uint32), ("ctas_per_sm_global", ctypes.c_uint32),
-                ("regs_per_thread", ctypes.c_uint32), ("smem_region_max", ctypes.c_uint64)]
+                ("regs_per_thread", ctypes.c_uint32), ("smem_region_max", ctypes.c_uint64),
+                ("ilp_smem", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

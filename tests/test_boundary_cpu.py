@@ -5,6 +5,7 @@ import ctypes
 import numpy as np
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -40,10 +41,26 @@ def test_strerror_and_codes(lib):
     assert sage.strerror(-4) == "CUDA error"
 
 
-def test_header_matches_binding_structs():
-    # sage_result / sage_config layouts as declared in sage.h
-    assert ctypes.sizeof(sage.sage_config) == 4 + 4 * 4 + 8 + 4  # int + 4 u32 + pad + void*
-    assert ctypes.sizeof(sage.sage_result) == 5 * 8 + 4 * 4
+def test_header_matches_binding_structs(tmp_path):
+    """The ctypes structs have the sizes and field offsets a C compiler gives the
+    structs declared in include/sage.h."""
+    structs = {"sage_config": sage.sage_config, "sage_result": sage.sage_result, "sage_info": sage.sage_info}
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "sage.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append('printf("%s %%zu\\n", sizeof(%s));' % (name, name))
+        for f, _ in cls._fields_:
+            lines.append('printf("%s.%s %%zu\\n", offsetof(%s, %s));' % (name, f, name, f))
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                   check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got["%s.%s" % (name, f)]) == getattr(cls, f).offset, (name, f)
 
 
 def test_init_argument_validation_without_device(lib):

@@ -216,13 +216,32 @@ def test_async_and_host_forms(dev):
 
 
 def test_occupancy_and_registers(dev):
-    """Full occupancy: 2 CTAs x 1024 threads per SM, <= 32 registers."""
+    """Full occupancy: 2048 logical threads per SM and the whole 64 K
+    register file allocated -- 2 CTAs x 1024 threads x 32 registers, or (the P=1
+    SMEM kernel, ILP 2) 1 CTA x 1024 threads x 2 lane states x 64 registers."""
     for P in (1, 4, 8):
         with sage.Context(pick_words=P) as ctx:
             info = ctx.query()
             assert info.threads == 1024 and info.blocks == 2 * info.sm_count
-            assert info.ctas_per_sm_smem == 2 and info.ctas_per_sm_global == 2
-            assert info.regs_per_thread <= 32
+            assert info.ilp_smem == (2 if P == 1 else 1)
+            assert info.ctas_per_sm_smem * info.ilp_smem == 2 and info.ctas_per_sm_global == 2
+            assert info.ctas_per_sm_smem * info.threads * info.regs_per_thread == 65536
+
+
+def test_ilp2_and_ilp1_kernels_agree(dev):
+    """The c2a kernel (ILP 2, one CTA per SM) and the ILP 1 kernel it falls back to
+    (odd block count) compute the same SCS-2 result for the same logical threads."""
+    region = torch.from_numpy(make_region(8192)).to(dev)
+    for blocks in (2, 4):
+        with sage.Context(blocks=blocks, threads=1024) as ctx:
+            a = ctx.attest(0xC2A, region, 300)
+        assert a.ilp == 2
+        want = oracle.attest(0xC2A, region.cpu().numpy(), region.data_ptr(), 300, blocks, 1024, 1)
+        assert a.checksum == want
+    with sage.Context(blocks=3, threads=1024) as ctx:
+        b = ctx.attest(0xC2A, region, 300)
+    assert b.ilp == 1
+    assert b.checksum == oracle.attest(0xC2A, region.cpu().numpy(), region.data_ptr(), 300, 3, 1024, 1)
 
 
 def test_argument_errors(dev):

@@ -69,15 +69,22 @@ def test_registers_allow_two_ctas_of_1024(res_usage):
             regs[name] = int(m.group(1))
     ks = {n: r for n, r in regs.items() if n.startswith("_ZN4sage20sage_checksum_kernel")}
     assert ks
+    ilp2 = [n for n in ks if n.endswith("ELi2ELi0ELi10EEEvNS_10KernelArgsE")]   # <..., ILP=2, PROBE=0, PAD=10>
+    assert len(ilp2) == 1, ilp2
     for n, r in ks.items():
-        if n.endswith("ILi2EEEvNS_10KernelArgsE"):       # ILP=2 variants (not instantiated in the product)
-            continue
-        assert r <= 32, (n, r)
+        if n in ilp2:
+            # one CTA of 1024 threads per SM must allocate the whole 64 K register file
+            assert r == 64, (n, r)
+        else:
+            assert r <= 32, (n, r)
 
 
-def test_c2a_kernel_op_mix():
-    """The c2a product kernel (P=1, SMEM, non-straddling, XS=16, ADDR=4): per
-    unrolled round at most 30 ALU-pipe and 26 FMA-pipe instructions (one of them
+@pytest.mark.parametrize("name,rounds", [("ILi1ELb1ELb0ELi16ELi16ELi4ELi0ELi0ELb0ELi0ELi2ELi0ELi10E", 32),
+                                         ("ILi1ELb1ELb0ELi16ELi32ELi4E", 32)])
+def test_c2a_kernel_op_mix(name, rounds):
+    """The c2a product kernels (P=1, SMEM, non-straddling, XS=16, ADDR=4; ILP=2
+    with 16 unrolled rounds of two lane states, and the ILP=1 fallback with 32):
+    per logical round at most 30 ALU-pipe and 26 FMA-pipe instructions (one of them
     the IMAD.WIDE of x*M64), one LDS and one SHFL.IDX -- the minimum ALU count
     for SCS-2's shift/xor/rotate steps (DESIGN.md sections 7-8)."""
     import os
@@ -85,10 +92,10 @@ def test_c2a_kernel_op_mix():
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
     import sass_loop
     build.build()
-    res = sass_loop.analyse(build.CUBIN, "ILi1ELb1ELb0ELi16ELi32ELi4E")
+    res = sass_loop.analyse(build.CUBIN, name)
     assert len(res) == 1, sorted(res)
     (d,) = res.values()
-    assert d["rounds"] == 32
+    assert d["rounds"] == rounds
     assert d["alu"] <= 30.1, d
     assert d["fma"] <= 26.1 and d["wide"] == 1.0, d
-    assert d["hist"].get("LDS", 0) == 32 and d["hist"].get("SHFL.IDX", 0) == 32, d
+    assert d["hist"].get("LDS", 0) == rounds and d["hist"].get("SHFL.IDX", 0) == rounds, d
