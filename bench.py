@@ -333,7 +333,9 @@ def run_ours(args):
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": {"workload": args.config, "desc": desc, "region_bytes": nbytes, "P": P, "rounds": R,
                            "blocks": info.blocks, "threads": info.threads, "threads_total": n,
-                           "placement": placement, "parallelism": "independent replica per GPU x%d" % ws,
+                           "placement": placement, "lane_states_per_thread": dbg.ilp,
+                           "hw_grid": "%d x %d" % (info.blocks // dbg.ilp, info.threads),
+                           "parallelism": "independent replica per GPU x%d" % ws,
                            "plumbing": backend or "none",
                            "l2": "256 MiB buffer written between timed steps (flush)"},
                 "checksummed_gbps": value * 4 * P / 1e9,

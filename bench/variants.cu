@@ -41,12 +41,14 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                   sage::sage_checksum_kernel<1, true, false, 16, 32, 4, 0, 0, false, 0, 1, PR>, 1, true, false, 1, 0, 0, PR}
 #define VARQ(U, ILP, PAD, T) {"P1 smem xs16 unroll" #U " addr4 ILP" #ILP " PAD" #PAD " T" #T, \
                   sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, 0, false, 0, ILP, 0, PAD>, 1, true, false, ILP, 0, 0, 0, T}
+#define VARS(U, PR, PAD) {"P1 smem xs16 unroll" #U " addr4 ILP2 PROBE" #PR " PAD" #PAD, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, 0, false, 0, 2, PR, PAD>, 1, true, false, 2}
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARA(1, true, false, 16, 32, 4), VARQ(16, 2, 0, 1024), VARQ(16, 2, 8, 1024), VARQ(16, 2, 10, 1024),
-    VARQ(8, 4, 0, 512), VARQ(4, 4, 0, 512), VARQ(8, 4, 0, 256), VARQ(16, 2, 0, 512),
+    VARA(1, true, false, 16, 32, 4), VARS(16, 0, 10), VARS(16, 4, 10), VARS(16, 12, 10), VARS(8, 4, 10),
+    VARS(16, 4, 0), VARS(16, 12, 0),
 };
 
 int main(int argc, char** argv) {

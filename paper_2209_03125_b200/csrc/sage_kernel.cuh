@@ -411,7 +411,10 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //   PROBE    measurement-only instruction-mix probes (never in the product; the
 //            checksum is then not SCS-2): bit 0 replaces the pick's shared-memory
 //            load by its address (ADDR == 4 only), bit 1 the neighbour exchange by
-//            the lane's own t, so the loop keeps only its integer arithmetic
+//            the lane's own t, so the loop keeps only its integer arithmetic;
+//            bit 2 (result-neutral, ILP > 1) staggers the lane states: each state's
+//            round starts with x += a'[0] * 0 (bit 3: a'[8]) on the other state's
+//            accumulator, an FMA-pipe dependency that offsets the two chains
 //   PAD      registers reserved (kept live across the round loop, unused) so that
 //            an ILP > 1 kernel allocates the whole register file
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
@@ -510,10 +513,17 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
 #pragma unroll
-            for (int s = 0; s < ILP; ++s)
+            for (int s = 0; s < ILP; ++s) {
+                if constexpr (ILP > 1 && (PROBE & 4)) {
+                    // stagger: a result-neutral FMA-pipe dependency (x += a'[K] * 0) on a
+                    // value the other lane state produces early in its last round
+                    constexpr int kDep = (PROBE & 8) ? 8 : 0;
+                    xlo[s] = a[(s + ILP - 1) % ILP][kDep] * args.zero + xlo[s];
+                }
                 scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(
                     a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
                     EVERY > 0 ? (u % EVERY == 0) : (u == 0));
+            }
         }
     }
     for (; r < rounds; ++r) {
