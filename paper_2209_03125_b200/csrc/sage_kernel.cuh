@@ -1,8 +1,9 @@
 // sage_kernel.cuh -- the SCS-2 checksum kernel for sm_100a.
 //
-// One launch = one attestation (SAGE section 5.2.2).  Every thread
-// of a full-occupancy grid (2 CTAs x 1024 threads per SM, 32 registers, the
-// B200 analogue of P:612-613) seeds its state from the nonce, runs R rounds of
+// One launch = one attestation (SAGE section 5.2.2).  Every logical
+// thread of a full-occupancy grid (2048 per SM: 2 CTAs x 1024 threads at 32
+// registers, or -- the c2a kernel -- 1 CTA x 1024 threads x 2 lane states at 64
+// registers; the B200 analogue of P:612-613) seeds its state from the nonce, runs R rounds of
 // SCS-2 entirely in registers, and the folded states are
 // reduced warp (shuffle) -> block (shared memory) -> grid (one 64-bit atomic
 // per CTA).
