@@ -46,9 +46,15 @@ extern "C" {
 #define SAGE_ECUDA        -4  /* CUDA runtime error; detail in sage_last_error() */
 
 /* region placement */
-#define SAGE_AUTO   0u  /* SMEM when the region fits at the launch's occupancy, else GLOBAL */
+#define SAGE_AUTO   0u  /* SMEM up to 64 KiB; HYBRID up to 1 MiB where allowed; else GLOBAL */
 #define SAGE_SMEM   1u  /* region staged once per CTA into shared memory (TMA bulk copy) */
 #define SAGE_GLOBAL 2u  /* region read in place from L2/HBM every round */
+#define SAGE_HYBRID 3u  /* first min(region, 192 KiB) staged in shared memory, the rest read
+                           in place; each pick loads from whichever holds it.  Needs P = 1,
+                           1024-thread blocks, an even block count and a region whose chunk
+                           addresses share their high 32 bits (one CTA x 1024 threads x 2
+                           lane states per SM); SAGE_AUTO picks it for 64 KiB < region <=
+                           1 MiB when those hold */
 
 typedef struct sage_ctx sage_ctx;
 
@@ -57,7 +63,7 @@ typedef struct {
     uint32_t blocks;      /* grid size; 0 => 2 * SM count (full occupancy) */
     uint32_t threads;     /* block size, multiple of 32, <= 1024; 0 => 1024 */
     uint32_t pick_words;  /* P, words read per round: 1, 4 or 8; 0 => 1 */
-    uint32_t placement;   /* SAGE_AUTO | SAGE_SMEM | SAGE_GLOBAL */
+    uint32_t placement;   /* SAGE_AUTO | SAGE_SMEM | SAGE_GLOBAL | SAGE_HYBRID */
     void*    stream;      /* cudaStream_t to launch on (borrowed); NULL => ctx-owned stream */
 } sage_config;
 
@@ -67,7 +73,7 @@ typedef struct {
     uint64_t elapsed_ns;  /* host CLOCK_MONOTONIC from before launch to result on host (t1 - t0) */
     uint64_t device_ns;   /* %globaltimer: last CTA end - first CTA start */
     uint64_t region_va;   /* device VA the region was read from (the `base` of SCS-2) */
-    uint32_t placement;   /* SAGE_SMEM or SAGE_GLOBAL actually used */
+    uint32_t placement;   /* SAGE_SMEM, SAGE_GLOBAL or SAGE_HYBRID actually used */
     uint32_t blocks;      /* grid actually launched */
     uint32_t threads;     /* block size actually launched */
     uint32_t pick_words;  /* P actually used */
@@ -96,7 +102,8 @@ int sage_checksum_init(const sage_config* cfg, sage_ctx** out);
  * region_bytes = 4 * P * Nc with Nc a power of two (<= 2^32); region 16-byte
  * aligned (32-byte for P = 8); rounds < 2^32.  Returns when the result is on
  * the host.  SAGE_EINVAL on a violated precondition or NULL pointer;
- * SAGE_EUNSUPPORTED when SAGE_SMEM was forced and the region does not fit. */
+ * SAGE_EUNSUPPORTED when SAGE_SMEM was forced and the region does not fit, or
+ * SAGE_HYBRID was forced without its geometry (see SAGE_HYBRID). */
 int sage_attest(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
                 uint64_t rounds, sage_result* out);
 
@@ -149,7 +156,8 @@ int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, siz
  * precompute the expected checksum ahead of time. */
 int sage_host_region_va(sage_ctx* ctx, size_t region_bytes, uint64_t* va_out);
 
-/* Placement the context would choose for region_bytes (SAGE_SMEM/SAGE_GLOBAL). */
+/* Placement the context would choose for region_bytes (SAGE_SMEM/SAGE_GLOBAL/SAGE_HYBRID;
+ * a HYBRID region whose chunk addresses straddle a 4 GiB boundary runs GLOBAL). */
 int sage_placement_for(sage_ctx* ctx, size_t region_bytes, uint32_t* placement_out);
 
 int sage_query(sage_ctx* ctx, sage_info* out);

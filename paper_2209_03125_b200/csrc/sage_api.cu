@@ -42,6 +42,11 @@ uint64_t now_ns() {
 }
 
 constexpr size_t kSmemRegionMax = 64 * 1024;   // 2 CTAs/SM x 64 KiB fits the 228 KB SM
+// SAGE_HYBRID: one CTA per SM stages the region's first 192 KiB; larger stages starve
+// L1 for the rest (224 KiB: 2x slower), smaller ones stage too little (measured at
+// 512 KiB: 128 / 160 / 192 KiB -> 91.4 / 79.0 / 74.1 ms vs 89-90 ms GLOBAL,
+// profiles/r01/variants/hybrid_placement*.jsonl).  AUTO uses it up to 1 MiB.
+constexpr size_t kHybridStage = 192 * 1024, kHybridRegionMax = 1024 * 1024;
 
 using KernelFn = void (*)(const sage::KernelArgs);
 
@@ -80,6 +85,12 @@ constexpr int kIlpSmem = 2, kIlpPad = 10, kIlpUnroll = 16;
 
 uint32_t ilp_for(uint32_t P, bool smem, bool straddle, uint32_t blocks, uint32_t threads) {
     return (P == 1 && smem && !straddle && threads == 1024 && blocks % kIlpSmem == 0) ? kIlpSmem : 1;
+}
+
+// SAGE_HYBRID kernel: ILP 2 as above, 4 unrolled rounds, 4 reserved registers (64 in all).
+constexpr int kHybridUnroll = 4, kHybridPad = 4;
+KernelFn hybrid_kernel() {
+    return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 7, 0, 0, false, 0, kIlpSmem, 0, kHybridPad>;
 }
 
 template <int P>
@@ -158,31 +169,48 @@ int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t round
 // SAGE_AUTO: SMEM when the region fits at 2 CTAs/SM, except P = 8, whose
 // random 32-B picks conflict heavily in shared-memory banks and run faster
 // from L1 (measured: 1510 vs 1843 cycles per round at 8 KiB).
+bool hybrid_geometry(const sage_ctx* c) {
+    return c->pick_words == 1 && c->threads == 1024 && c->blocks % kIlpSmem == 0;
+}
+
 uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
     if (c->placement != SAGE_AUTO) return c->placement;
     if (c->pick_words == 8) return SAGE_GLOBAL;
-    return bytes <= kSmemRegionMax ? SAGE_SMEM : SAGE_GLOBAL;
+    if (bytes <= kSmemRegionMax) return SAGE_SMEM;
+    if (bytes <= kHybridRegionMax && hybrid_geometry(c)) return SAGE_HYBRID;
+    return SAGE_GLOBAL;
 }
 
 int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
            uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
-    const uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
+    uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
     if (placement == SAGE_SMEM && bytes > kSmemRegionMax)
         return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s", "64 KiB");
-    const bool smem = placement == SAGE_SMEM;
     const uint64_t lo = reinterpret_cast<uint64_t>(region);
     const bool straddle = (lo >> 32) != ((lo + bytes - 1) >> 32);
-    const uint32_t ilp = counts ? 1 : ilp_for(c->pick_words, smem, straddle, c->blocks, c->threads);
+    if (placement == SAGE_HYBRID && (!hybrid_geometry(c) || straddle)) {
+        if (c->placement == SAGE_HYBRID)
+            return fail(SAGE_EUNSUPPORTED, "SAGE_HYBRID needs P=1, 1024-thread blocks, an even block count and a "
+                                           "region inside one 4 GiB window%s");
+        placement = SAGE_GLOBAL;                    // AUTO: a straddling region runs GLOBAL
+    }
+    const bool hybrid = placement == SAGE_HYBRID;
+    const bool smem = placement == SAGE_SMEM;
+    uint32_t ilp = counts ? 1 : ilp_for(c->pick_words, smem, straddle, c->blocks, c->threads);
     KernelFn fn = counts ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle, ilp);
-    const size_t dyn = smem ? bytes : 0;
-    if (smem) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+    if (hybrid) {
+        ilp = kIlpSmem;
+        fn = hybrid_kernel();
+    }
+    const size_t dyn = smem ? bytes : hybrid ? (bytes < kHybridStage ? bytes : kHybridStage) : 0;
+    if (dyn) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
     sage::KernelArgs args{};
     args.region = static_cast<const uint32_t*>(region);
     args.nonce = nonce;
     args.nc_mask = static_cast<uint32_t>(bytes / (4ull * c->pick_words) - 1);
     args.rounds = static_cast<uint32_t>(rounds);
-    args.region_bytes = static_cast<uint32_t>(smem ? bytes : 0);
+    args.region_bytes = static_cast<uint32_t>(dyn);   // bytes staged in shared memory
     args.raw = raw;
     args.per_warp = per_warp;
     args.counts = counts;
@@ -249,7 +277,7 @@ int sage_checksum_init(const sage_config* cfg, sage_ctx** out) {
     if (d.threads % 32 != 0 || d.threads > 1024) return fail(SAGE_EINVAL, "threads must be a multiple of 32, <= 1024%s");
     if (d.pick_words != 1 && d.pick_words != 4 && d.pick_words != 8)
         return fail(SAGE_EINVAL, "pick_words must be 1, 4 or 8%s");
-    if (d.placement > SAGE_GLOBAL) return fail(SAGE_EINVAL, "unknown placement%s");
+    if (d.placement > SAGE_HYBRID) return fail(SAGE_EINVAL, "unknown placement%s");
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (d.device < 0 || d.device >= ndev) return fail(SAGE_EINVAL, "device ordinal out of range%s");

@@ -16,8 +16,8 @@ SAGE_EUNSUPPORTED = -2
 SAGE_ENOMEM = -3
 SAGE_ECUDA = -4
 
-SAGE_AUTO, SAGE_SMEM, SAGE_GLOBAL = 0, 1, 2
-PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto"}
+SAGE_AUTO, SAGE_SMEM, SAGE_GLOBAL, SAGE_HYBRID = 0, 1, 2, 3
+PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto", SAGE_HYBRID: "hybrid"}
 
 # every symbol include/sage.h declares
 EXPORTS = ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",

@@ -395,3 +395,78 @@ def test_full_occupancy_wide_picks_sampled(dev, P):
     assert sum(parts) & M64 == res.checksum
     for w in (0, n // 96, n // 32 - 1):
         assert parts[w] == oracle.warp_sum(0xE0 + P, region, d.data_ptr(), R, w, P), w
+
+
+@pytest.mark.parametrize("nbytes", [128 << 10, 256 << 10, 512 << 10, 1 << 20])
+def test_hybrid_placement_bit_exact(dev, nbytes):
+    """SAGE_HYBRID (first 192 KiB in shared memory, the rest read in place): chosen by
+    SAGE_AUTO for 64 KiB < region <= 1 MiB at a 1024-thread, even-block geometry, and
+    bit-exact with the oracle and with the GLOBAL placement."""
+    region = make_region(nbytes, prefix=kernel_code_prefix(1, False), fill_seed=nbytes)
+    d, _keep = to_dev(region, dev, align_offset=16)
+    out = {}
+    for placement in (sage.SAGE_AUTO, sage.SAGE_GLOBAL):
+        with sage.Context(blocks=2, threads=1024, placement=placement) as ctx:
+            res = ctx.attest(0x48B, d, 200)
+            out[placement] = res
+    assert out[sage.SAGE_AUTO].placement == sage.SAGE_HYBRID and out[sage.SAGE_AUTO].ilp == 2
+    assert out[sage.SAGE_GLOBAL].placement == sage.SAGE_GLOBAL
+    want = oracle.attest(0x48B, region, d.data_ptr(), 200, 2, 1024, 1)
+    assert out[sage.SAGE_AUTO].checksum == out[sage.SAGE_GLOBAL].checksum == want
+
+
+def test_hybrid_forced_small_region_and_unsupported_geometry(dev):
+    """Forced SAGE_HYBRID on an 8 KiB region stages all of it; without its geometry
+    (P = 1, 1024-thread blocks, even block count) it is SAGE_EUNSUPPORTED."""
+    region = make_region(8192)
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=4, threads=1024, placement=sage.SAGE_HYBRID) as ctx:
+        res = ctx.attest(5, d, 150)
+    assert res.placement == sage.SAGE_HYBRID
+    assert res.checksum == oracle.attest(5, region, d.data_ptr(), 150, 4, 1024, 1)
+    for kw in ({"blocks": 2, "threads": 512}, {"blocks": 3, "threads": 1024}):
+        with sage.Context(placement=sage.SAGE_HYBRID, **kw) as ctx:
+            with pytest.raises(sage.SageError) as e:
+                ctx.attest(5, d, 10)
+            assert e.value.code == sage.SAGE_EUNSUPPORTED
+    with sage.Context(blocks=2, threads=1024) as ctx:     # AUTO at other geometries: GLOBAL
+        assert ctx.placement_for(512 << 10) == sage.SAGE_HYBRID
+        assert ctx.placement_for(2 << 20) == sage.SAGE_GLOBAL
+    with sage.Context(blocks=3, threads=1024) as ctx:
+        assert ctx.placement_for(512 << 10) == sage.SAGE_GLOBAL
+
+
+def test_hybrid_straddling_region_runs_global(dev):
+    """A 512 KiB region whose chunk addresses straddle a 4 GiB boundary cannot use the
+    hybrid kernel's 32-bit data pointer; SAGE_AUTO runs it GLOBAL, bit-exact."""
+    big = torch.empty((4 << 30) + (2 << 20), dtype=torch.uint8, device=dev)
+    base0 = big.data_ptr()
+    boundary = ((base0 >> 32) + 1) << 32
+    nbytes = 512 << 10
+    start = boundary - nbytes // 2 - base0
+    d = big[start:start + nbytes]
+    region = make_region(nbytes, fill_seed=77)
+    d.copy_(torch.from_numpy(region))
+    with sage.Context(blocks=2, threads=1024) as ctx:
+        res = ctx.attest(77, d, 100)
+    assert res.placement == sage.SAGE_GLOBAL
+    assert res.checksum == oracle.attest(77, region, d.data_ptr(), 100, 2, 1024, 1)
+    del big
+
+
+def test_paper_buffer_full_occupancy_sampled(dev):
+    """c2c as bench.py times it: the paper's 524,288-B buffer at full
+    occupancy (SAGE_HYBRID), 10^5 rounds; sum consistency plus sampled warps."""
+    region = make_region(512 << 10, prefix=kernel_code_prefix(1, False))
+    d, _keep = to_dev(region, dev)
+    R = 100_000
+    with sage.Context() as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
+        res = ctx.attest_debug(0xC2C, d, R, pw)
+    assert res.placement == sage.SAGE_HYBRID
+    parts = [int(v) & M64 for v in pw.cpu().tolist()]
+    assert sum(parts) & M64 == res.checksum
+    for w in (0, 1, n // 64, n // 32 - 1):
+        assert parts[w] == oracle.warp_sum(0xC2C, region, d.data_ptr(), R, w, 1), w
