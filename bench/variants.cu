@@ -47,12 +47,14 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                   sage::sage_checksum_kernel<P, false, true, 16, U, 0, 0, 0, false, 0, ILP, 0, PAD>, P, false, true, ILP}
 #define VARHP(P, U, ST, PAD) {"P" #P " hybrid unroll" #U " ILP2 stage" #ST " PAD" #PAD, \
                   sage::sage_checksum_kernel<P, true, false, 16, U, 7, 0, 0, false, 0, 2, 0, PAD>, P, true, false, 2, 0, ST}
+#define VARH8(U, ST, PAD) {"P1 hybrid8 unroll" #U " ILP2 stage" #ST " PAD" #PAD, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 8, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2, 0, ST}
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
 static V variants[] = {
-    VARGI(1, 16, 1, 0), VARHP(1, 1, 196608, 0), VARHP(1, 4, 196608, 0), VARHP(1, 4, 163840, 0),
-    VARHP(1, 4, 131072, 0), VARHP(1, 8, 196608, 0), VARGI(1, 16, 1, 0),
+    VARGI(1, 16, 1, 0), VARH8(2, 196608, 0), VARH8(2, 196608, 4), VARH8(2, 196608, 6), VARH8(2, 196608, 8),
+    VARH8(1, 196608, 6), VARH8(4, 196608, 0), VARGI(1, 16, 1, 0),
 };
 
 int main(int argc, char** argv) {

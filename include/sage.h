@@ -46,14 +46,16 @@ extern "C" {
 #define SAGE_ECUDA        -4  /* CUDA runtime error; detail in sage_last_error() */
 
 /* region placement */
-#define SAGE_AUTO   0u  /* SMEM up to 64 KiB; HYBRID up to 1 MiB where allowed; else GLOBAL */
+#define SAGE_AUTO   0u  /* SMEM up to smem_region_max (64 KiB, or 128 KiB at the ILP-2 geometry:
+                           P = 1, 1024-thread blocks, even block count); then HYBRID up to
+                           1 MiB at that geometry; else GLOBAL */
 #define SAGE_SMEM   1u  /* region staged once per CTA into shared memory (TMA bulk copy) */
 #define SAGE_GLOBAL 2u  /* region read in place from L2/HBM every round */
 #define SAGE_HYBRID 3u  /* first min(region, 192 KiB) staged in shared memory, the rest read
                            in place; each pick loads from whichever holds it.  Needs P = 1,
                            1024-thread blocks, an even block count and a region whose chunk
                            addresses share their high 32 bits (one CTA x 1024 threads x 2
-                           lane states per SM); SAGE_AUTO picks it for 64 KiB < region <=
+                           lane states per SM); SAGE_AUTO picks it for 128 KiB < region <=
                            1 MiB when those hold */
 
 typedef struct sage_ctx sage_ctx;
@@ -89,7 +91,8 @@ typedef struct {
     uint32_t ctas_per_sm_smem; /* resident CTAs/SM of the SMEM kernel with a 64 KiB region */
     uint32_t ctas_per_sm_global;
     uint32_t regs_per_thread;  /* of the P-specific SMEM kernel */
-    uint64_t smem_region_max;  /* largest region (bytes) SAGE_AUTO stages into SMEM */
+    uint64_t smem_region_max;  /* largest region (bytes) SAGE_AUTO stages into SMEM: 64 KiB,
+                                  128 KiB at the ILP-2 geometry (see SAGE_AUTO) */
     uint32_t ilp_smem;         /* lane states per thread of that SMEM kernel (1 or 2) */
 } sage_info;
 

@@ -42,10 +42,15 @@ uint64_t now_ns() {
 }
 
 constexpr size_t kSmemRegionMax = 64 * 1024;   // 2 CTAs/SM x 64 KiB fits the 228 KB SM
+// With the ILP 2 kernel (one CTA per SM) a 128 KiB region still fits in shared memory
+// (measured 54.8 ms vs 60.2 ms GLOBAL at 128 KiB).
+constexpr size_t kSmemRegionMaxIlp2 = 128 * 1024;
 // SAGE_HYBRID: one CTA per SM stages the region's first 192 KiB; larger stages starve
 // L1 for the rest (224 KiB: 2x slower), smaller ones stage too little (measured at
-// 512 KiB: 128 / 160 / 192 KiB -> 91.4 / 79.0 / 74.1 ms vs 89-90 ms GLOBAL,
-// profiles/r01/variants/hybrid_placement*.jsonl).  AUTO uses it up to 1 MiB.
+// 512 KiB: 128 / 160 / 192 KiB -> 91.4 / 79.0 / 74.1 ms vs 89-94 ms GLOBAL,
+// profiles/r01/variants/hybrid_placement*.jsonl).  AUTO uses it for 128 KiB < region
+// <= 1 MiB: 61.7 / 75.6 / 18.1 ms (R = 2e4) vs 64.0 / 93.7 / 18.8 ms GLOBAL at
+// 256 KiB / 512 KiB / 1 MiB.
 constexpr size_t kHybridStage = 192 * 1024, kHybridRegionMax = 1024 * 1024;
 
 using KernelFn = void (*)(const sage::KernelArgs);
@@ -87,10 +92,11 @@ uint32_t ilp_for(uint32_t P, bool smem, bool straddle, uint32_t blocks, uint32_t
     return (P == 1 && smem && !straddle && threads == 1024 && blocks % kIlpSmem == 0) ? kIlpSmem : 1;
 }
 
-// SAGE_HYBRID kernel: ILP 2 as above, 4 unrolled rounds, 4 reserved registers (64 in all).
-constexpr int kHybridUnroll = 4, kHybridPad = 4;
+// SAGE_HYBRID kernel: ILP 2 as above, addressing on the FMA pipe (ADDR 8), 2 unrolled
+// rounds, 8 reserved registers (64 in all).
+constexpr int kHybridUnroll = 2, kHybridPad = 8;
 KernelFn hybrid_kernel() {
-    return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 7, 0, 0, false, 0, kIlpSmem, 0, kHybridPad>;
+    return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 8, 0, 0, false, 0, kIlpSmem, 0, kHybridPad>;
 }
 
 template <int P>
@@ -169,14 +175,17 @@ int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t round
 // SAGE_AUTO: SMEM when the region fits at 2 CTAs/SM, except P = 8, whose
 // random 32-B picks conflict heavily in shared-memory banks and run faster
 // from L1 (measured: 1510 vs 1843 cycles per round at 8 KiB).
+// The geometry of the ILP 2 kernels (c2a SMEM and SAGE_HYBRID).
 bool hybrid_geometry(const sage_ctx* c) {
     return c->pick_words == 1 && c->threads == 1024 && c->blocks % kIlpSmem == 0;
 }
 
+size_t smem_region_max(const sage_ctx* c) { return hybrid_geometry(c) ? kSmemRegionMaxIlp2 : kSmemRegionMax; }
+
 uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
     if (c->placement != SAGE_AUTO) return c->placement;
     if (c->pick_words == 8) return SAGE_GLOBAL;
-    if (bytes <= kSmemRegionMax) return SAGE_SMEM;
+    if (bytes <= smem_region_max(c)) return SAGE_SMEM;
     if (bytes <= kHybridRegionMax && hybrid_geometry(c)) return SAGE_HYBRID;
     return SAGE_GLOBAL;
 }
@@ -184,10 +193,18 @@ uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
 int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
            uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
     uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
-    if (placement == SAGE_SMEM && bytes > kSmemRegionMax)
-        return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s", "64 KiB");
+    if (placement == SAGE_SMEM && bytes > smem_region_max(c))
+        return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s",
+                    hybrid_geometry(c) ? "128 KiB" : "64 KiB");
     const uint64_t lo = reinterpret_cast<uint64_t>(region);
     const bool straddle = (lo >> 32) != ((lo + bytes - 1) >> 32);
+    if (placement == SAGE_SMEM && straddle && bytes > kSmemRegionMax) {
+        // beyond 64 KiB only the ILP 2 kernel keeps full occupancy, and it needs the
+        // 32-bit data pointer of a non-straddling region
+        if (c->placement == SAGE_SMEM)
+            return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM: a region over 64 KiB must not straddle a 4 GiB boundary%s");
+        placement = SAGE_GLOBAL;
+    }
     if (placement == SAGE_HYBRID && (!hybrid_geometry(c) || straddle)) {
         if (c->placement == SAGE_HYBRID)
             return fail(SAGE_EUNSUPPORTED, "SAGE_HYBRID needs P=1, 1024-thread blocks, an even block count and a "
@@ -435,7 +452,7 @@ int sage_query(sage_ctx* ctx, sage_info* out) {
     info.threads = ctx->threads;
     info.pick_words = ctx->pick_words;
     info.placement = ctx->placement;
-    info.smem_region_max = kSmemRegionMax;
+    info.smem_region_max = smem_region_max(ctx);
     const uint32_t ilp = ilp_for(ctx->pick_words, true, false, ctx->blocks, ctx->threads);
     info.ilp_smem = ilp;
     KernelFn fs = kernel_for(ctx->pick_words, true, false, ilp), fg = kernel_for(ctx->pick_words, false, true);

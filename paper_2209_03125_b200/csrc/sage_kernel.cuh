@@ -347,6 +347,21 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                          : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
         }
         t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 8) {
+        // hybrid placement as ADDR == 7 with the address arithmetic on the FMA pipe:
+        // shared address and 64-bit global address as IMAD / IMAD.WIDE, and the R6
+        // bracket folded as in ADDR == 4
+        const uint32_t saddr = i * args.four_p + smem_u32(smem_words);
+        const uint64_t gaddr = static_cast<uint64_t>(i) * args.four_p + base;
+        const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
+        const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        static_assert(P == 1, "ADDR 8 is the P = 1 hybrid form");
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "setp.lt.u32 p, %1, %2;\n\t"
+                     "@p ld.shared.b32 %0, [%3];\n\t"
+                     "@!p ld.global.nc.b32 %0, [%4];\n\t}"
+                     : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 5) {
         // lo32(y) + 4P*i in one IMAD, then the warp-uniform bracket
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);

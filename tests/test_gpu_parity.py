@@ -397,10 +397,30 @@ def test_full_occupancy_wide_picks_sampled(dev, P):
         assert parts[w] == oracle.warp_sum(0xE0 + P, region, d.data_ptr(), R, w, P), w
 
 
-@pytest.mark.parametrize("nbytes", [128 << 10, 256 << 10, 512 << 10, 1 << 20])
+def test_ilp2_smem_region_up_to_128k(dev):
+    """At the ILP-2 geometry (one CTA per SM) SAGE_AUTO stages regions up to 128 KiB in
+    shared memory; bit-exact with the oracle and with GLOBAL."""
+    region = make_region(128 << 10, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=2, threads=1024) as ctx:
+        assert ctx.query().smem_region_max == 128 << 10
+        assert ctx.placement_for(128 << 10) == sage.SAGE_SMEM
+        res = ctx.attest(0x128, d, 200)
+    assert res.placement == sage.SAGE_SMEM and res.ilp == 2
+    with sage.Context(blocks=2, threads=1024, placement=sage.SAGE_GLOBAL) as ctx:
+        glob = ctx.attest(0x128, d, 200)
+    assert res.checksum == glob.checksum == oracle.attest(0x128, region, d.data_ptr(), 200, 2, 1024, 1)
+    with sage.Context(blocks=2, threads=512, placement=sage.SAGE_SMEM) as ctx:   # ILP 1: 64 KiB at most
+        assert ctx.query().smem_region_max == 64 << 10
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(0x128, d, 10)
+        assert e.value.code == sage.SAGE_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("nbytes", [256 << 10, 512 << 10, 1 << 20])
 def test_hybrid_placement_bit_exact(dev, nbytes):
     """SAGE_HYBRID (first 192 KiB in shared memory, the rest read in place): chosen by
-    SAGE_AUTO for 64 KiB < region <= 1 MiB at a 1024-thread, even-block geometry, and
+    SAGE_AUTO for 128 KiB < region <= 1 MiB at a 1024-thread, even-block geometry, and
     bit-exact with the oracle and with the GLOBAL placement."""
     region = make_region(nbytes, prefix=kernel_code_prefix(1, False), fill_seed=nbytes)
     d, _keep = to_dev(region, dev, align_offset=16)
@@ -430,19 +450,21 @@ def test_hybrid_forced_small_region_and_unsupported_geometry(dev):
                 ctx.attest(5, d, 10)
             assert e.value.code == sage.SAGE_EUNSUPPORTED
     with sage.Context(blocks=2, threads=1024) as ctx:     # AUTO at other geometries: GLOBAL
-        assert ctx.placement_for(512 << 10) == sage.SAGE_HYBRID
+        assert ctx.placement_for(128 << 10) == sage.SAGE_SMEM
+        assert ctx.placement_for(256 << 10) == sage.SAGE_HYBRID
         assert ctx.placement_for(2 << 20) == sage.SAGE_GLOBAL
     with sage.Context(blocks=3, threads=1024) as ctx:
         assert ctx.placement_for(512 << 10) == sage.SAGE_GLOBAL
 
 
-def test_hybrid_straddling_region_runs_global(dev):
-    """A 512 KiB region whose chunk addresses straddle a 4 GiB boundary cannot use the
-    hybrid kernel's 32-bit data pointer; SAGE_AUTO runs it GLOBAL, bit-exact."""
+@pytest.mark.parametrize("nbytes", [128 << 10, 512 << 10])
+def test_ilp2_placements_straddling_region_run_global(dev, nbytes):
+    """A region over 64 KiB whose chunk addresses straddle a 4 GiB boundary cannot use
+    the ILP-2 kernels' 32-bit data pointer; SAGE_AUTO runs it GLOBAL, bit-exact, and
+    forcing SMEM / HYBRID is SAGE_EUNSUPPORTED."""
     big = torch.empty((4 << 30) + (2 << 20), dtype=torch.uint8, device=dev)
     base0 = big.data_ptr()
     boundary = ((base0 >> 32) + 1) << 32
-    nbytes = 512 << 10
     start = boundary - nbytes // 2 - base0
     d = big[start:start + nbytes]
     region = make_region(nbytes, fill_seed=77)
@@ -451,6 +473,11 @@ def test_hybrid_straddling_region_runs_global(dev):
         res = ctx.attest(77, d, 100)
     assert res.placement == sage.SAGE_GLOBAL
     assert res.checksum == oracle.attest(77, region, d.data_ptr(), 100, 2, 1024, 1)
+    forced = sage.SAGE_SMEM if nbytes <= (128 << 10) else sage.SAGE_HYBRID
+    with sage.Context(blocks=2, threads=1024, placement=forced) as ctx:
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(77, d, 10)
+        assert e.value.code == sage.SAGE_EUNSUPPORTED
     del big
 
 
