@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "checksum rounds/s and checksummed GB/s per B200 (1/2/4/8 GPU); p99 attest time"
 UNIT = "thread-rounds/s"
+CPU_SAMPLE_S = 10.0          # target wall time of the cpu_baseline sample (all host cores)
 
 # Algorithmic 32-bit integer operations per thread-round of SCS-2 (DESIGN.md
 # section 7): minimal sm_100 lowering with 3-input LOP3 / IMAD / LEA.HI.
@@ -300,7 +301,8 @@ def run_ours(args):
         t_e2e = replicas.max_over_ranks(time.perf_counter() - t0, pdev)
         e2e = {"value": ws * n * R * args.steps / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32,
-               "api": "sage_attest_host (pinned host region)"}
+               "api": "sage_attest_host (pinned host region)",
+               "l2": "not flushed: each step's H2D copy rewrites the region just before the kernel reads it"}
         ctx_h.close()
 
     # attestation wall time as the verifier sees it (sage_attest, device region)
@@ -371,9 +373,14 @@ def run_ours(args):
             cores = len(os.sched_getaffinity(0))
             host = region_np if region_np is not None else region.cpu().numpy()
             nw = n // 32
-            want = min(nw, 32 * cores)
-            sample = sorted(set(int(round(i * (nw - 1) / max(1, want - 1))) for i in range(want)))
+            def spread(k):
+                return sorted(set(int(round(i * (nw - 1) / max(1, k - 1))) for i in range(k)))
             with oracle.WarpPool(host, cores) as pool:
+                # size the sample for ~CPU_SAMPLE_S of wall time on all cores: a
+                # short calibration pass (one warp per core), then the timed sample
+                _, dt0, _ = cpu_oracle_rate(pool, 0x1234, region.data_ptr(), R, spread(min(nw, cores)), P)
+                want = max(min(nw, cores), min(nw, int(min(nw, cores) * CPU_SAMPLE_S / max(dt0, 1e-3))))
+                sample = spread(want)
                 rate, dt, sums = cpu_oracle_rate(pool, 0x1234, region.data_ptr(), R, sample, P)
             with oracle.WarpPool(host, 1) as pool1:             # one core, a smaller sample
                 rate1, dt1, sums1 = cpu_oracle_rate(pool1, 0x1234, region.data_ptr(), R, sample[:4], P)

@@ -52,9 +52,11 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 #define VARA(P, S, ST, XS, U, A) {"P" #P " smem" #S " straddle" #ST " xs" #XS " unroll" #U " addr" #A, \
                               sage::sage_checksum_kernel<P, S, ST, XS, U, A>, P, S, ST}
 
+#define VARY(U, SY) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD10 SYNC" #SY, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, 0, false, 0, 2, 0, 10, SY>, 1, true, false, 2}
+
 static V variants[] = {
-    VARGI(1, 16, 1, 0), VARH8(2, 196608, 0), VARH8(2, 196608, 4), VARH8(2, 196608, 6), VARH8(2, 196608, 8),
-    VARH8(1, 196608, 6), VARH8(4, 196608, 0), VARGI(1, 16, 1, 0),
+    VARY(16, 0), VARY(16, 1), VARY(16, 4), VARY(16, 16), VARY(16, 64), VARY(16, 256), VARY(16, 0),
 };
 
 int main(int argc, char** argv) {

@@ -433,13 +433,15 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //            accumulator, an FMA-pipe dependency that offsets the two chains
 //   PAD      registers reserved (kept live across the round loop, unused) so that
 //            an ILP > 1 kernel allocates the whole register file
+//   SYNC     > 0: a CTA barrier every SYNC trips of the round loop (result-neutral;
+//            bounds how far the warps of a CTA drift apart before the final reduction)
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
 //            CTA x 1024 threads per SM at 64 registers -- the same register file
 //            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
-          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0>
+          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0, int SYNC = 0>
 __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
@@ -525,7 +527,15 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
     // a10: round loop, UNROLL rounds per trip + remainder
     uint32_t r = 0;
     const uint32_t main_end = rounds - rounds % UNROLL;
+    uint32_t trips_to_sync = SYNC;
     for (; r < main_end; r += UNROLL) {
+        if constexpr (SYNC > 0) {
+            // keep the CTA's warps within SYNC trips of each other (result-neutral)
+            if (--trips_to_sync == 0) {
+                trips_to_sync = SYNC;
+                __syncthreads();
+            }
+        }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
 #pragma unroll
