@@ -40,7 +40,8 @@ CONFIGS = {
     "c1": (4096, 1, 10_000, "1 block x 32 threads, 4 KiB SMEM region, 1e4 rounds"),
     "c2a": (8192, 1, 100_000, "full occupancy, 8 KiB SMEM region (kernel code), 1e5 rounds"),
     "c2b": (65536, 1, 100_000, "full occupancy, 64 KiB SMEM region, 1e5 rounds"),
-    "c2c": (524288, 1, 100_000, "full occupancy, 512 KiB region in L2 (GLOBAL), 1e5 rounds"),
+    "c2c": (524288, 1, 100_000, "full occupancy, the paper's 512 KiB buffer (P:690): first 192 KiB staged in SMEM, "
+                                   "the rest read from L2 (SAGE_HYBRID), 1e5 rounds"),
     "c3p1": (256 << 20, 1, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=1, 1e4 rounds"),
     "c3p4": (256 << 20, 4, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=4, 1e4 rounds"),
     "c3p8": (256 << 20, 8, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=8, 1e4 rounds"),

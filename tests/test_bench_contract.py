@@ -1,0 +1,71 @@
+"""bench.py's output contract (the JSON line the driver parses): the oracle
+(reference) arm on CPU, and on a GPU our arm at N=1 and the N=2 torchrun path
+(two replicas sharing one GPU over gloo plumbing, 8(e))."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(args, timeout):
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, capture_output=True,
+                       text=True, timeout=timeout)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout                 # rank 0 prints exactly one JSON line
+    return json.loads(lines[0])
+
+
+def _check_base(line, n_gpus, steps, warmup):
+    assert BASE_KEYS <= set(line), BASE_KEYS - set(line)
+    assert line["metric"].startswith("checksum rounds/s")
+    assert line["unit"] == "thread-rounds/s" and line["higher_is_better"] is True
+    assert line["n_gpus"] == n_gpus and line["steps"] == steps and line["warmup"] == warmup
+    assert line["value"] > 0 and line["ms_per_step"] > 0
+    assert line["scaling"] == "weak" and line["vs_baseline"] is None
+    assert line["dtype"] == "u32" and line["data"] == "synthetic"
+    assert "workload" in line["config"]
+    e2e = line["e2e"]
+    assert e2e["value"] > 0 and e2e["unit"] == line["unit"]
+    assert "h2d_bytes_per_step" in e2e and "d2h_bytes_per_step" in e2e
+
+
+def test_reference_arm_on_cpu():
+    line = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3"], 600)
+    _check_base(line, 1, 2, 3)
+    assert line["impl"] == "reference"
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+@pytest.mark.gpu
+def test_our_arm_one_gpu():
+    line = _run(["--config", "c2a", "--rounds", "2000", "--steps", "4", "--warmup", "3"], 900)
+    _check_base(line, 1, 4, 3)
+    assert line["gpu_launches"] == 4                 # one checksum kernel per timed step
+    rf = line["roofline"]
+    assert rf["bound"] == "alu" and 0 < rf["frac"] <= 1 and rf["peak"] > 0
+    assert abs(rf["achieved"] / rf["peak"] - rf["frac"]) < 1e-9
+    assert line["e2e"]["h2d_bytes_per_step"] == 8192 and line["e2e"]["d2h_bytes_per_step"] == 32
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["parity_on_sample"] is True and cb["cores"] >= 1
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
+    assert line["attest_ms"]["p99"] >= line["attest_ms"]["p50"] > 0
+
+
+@pytest.mark.gpu
+def test_our_arm_two_replicas_torchrun():
+    line = _run(["--gpus", "2", "--config", "c2a", "--rounds", "2000", "--steps", "3", "--warmup", "3"], 900)
+    _check_base(line, 2, 3, 3)
+    reps = line["replicas"]
+    assert len(reps) == 2 and {r["rank"] for r in reps} == {0, 1}
+    assert reps[0]["nonce"] != reps[1]["nonce"]       # an independent nonce stream per replica
+    assert all(r["sampled_parity_sum_ok"] for r in reps)
+    assert "cpu_baseline" not in line                 # rank 0 at N=1 only
