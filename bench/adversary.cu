@@ -53,6 +53,13 @@ static K kernels[] = {
     {"ILP2 unpadded", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2>, 0, 0, 2},
     {"ILP2 unpadded +1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -1, false, 1, 2>, -1, 1, 2},
     {"ILP2 unpadded +1 instr / 16", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 16, 2>, 1, 16, 2},
+    // the adversary's own work in the issue slots the checksum leaves idle: a chain
+    // independent of the checksum state, FP32 FFMA (FEXTRA > 0) or integer IMAD (< 0)
+    {"+1 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 1>, 0, 1, 2},
+    {"+2 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 2>, 0, 1, 2},
+    {"+4 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 4>, 0, 1, 2},
+    {"+8 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 8>, 0, 1, 2},
+    {"+1 indep IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, -1>, 0, 1, 2},
 };
 
 static uint64_t now_ns() {

@@ -435,13 +435,18 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //            an ILP > 1 kernel allocates the whole register file
 //   SYNC     > 0: a CTA barrier every SYNC trips of the round loop (result-neutral;
 //            bounds how far the warps of a CTA drift apart before the final reduction)
+//   FEXTRA   timing adversary only (0 in the product): the adversary's own work
+//            alongside the checksum, |FEXTRA| dependent ops per round per lane
+//            state on a chain independent of the checksum state -- FFMA (FP32,
+//            either FMA pipe) for FEXTRA > 0, IMAD (FMA-heavy pipe) for FEXTRA < 0;
+//            folded into the result as (value & 0), so the checksum is unchanged
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
 //            CTA x 1024 threads per SM at 64 registers -- the same register file
 //            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
-          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0, int SYNC = 0>
+          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0, int SYNC = 0, int FEXTRA = 0>
 __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
@@ -528,6 +533,13 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
     uint32_t r = 0;
     const uint32_t main_end = rounds - rounds % UNROLL;
     uint32_t trips_to_sync = SYNC;
+    float fadv[ILP];                                   // FEXTRA > 0: the adversary's FP32 chain
+    uint32_t iadv[ILP];                                // FEXTRA < 0: the adversary's integer chain
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) {
+        fadv[s] = static_cast<float>(lane + s);
+        iadv[s] = lane + s;
+    }
     for (; r < main_end; r += UNROLL) {
         if constexpr (SYNC > 0) {
             // keep the CTA's warps within SYNC trips of each other (result-neutral)
@@ -549,6 +561,11 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
                 scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(
                     a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
                     EVERY > 0 ? (u % EVERY == 0) : (u == 0));
+#pragma unroll
+                for (int e = 0; e < (FEXTRA > 0 ? FEXTRA : -FEXTRA); ++e) {
+                    if constexpr (FEXTRA > 0) fadv[s] = fmaf(fadv[s], 1.0001f, 0.5f);
+                    else iadv[s] = iadv[s] * args.mul[e & 15] + args.one;
+                }
             }
         }
     }
@@ -559,6 +576,11 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
                                                                       args, policy, true);
     }
 
+    if constexpr (FEXTRA != 0) {
+#pragma unroll
+        for (int s = 0; s < ILP; ++s)          // keep the adversary's chain live: xlo ^= v & 0
+            xlo[s] ^= (FEXTRA > 0 ? __float_as_uint(fadv[s]) : iadv[s]) & args.zero;
+    }
     if constexpr (PAD > 0) {
 #pragma unroll
         for (int k = 0; k < PAD; ++k)          // xlo ^= pad & 0 (args.zero): result-neutral

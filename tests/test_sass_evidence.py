@@ -69,8 +69,8 @@ def test_registers_allow_two_ctas_of_1024(res_usage):
             regs[name] = int(m.group(1))
     ks = {n: r for n, r in regs.items() if n.startswith("_ZN4sage20sage_checksum_kernel")}
     assert ks
-    # <..., ILP=2, PROBE=0, PAD, SYNC=0>: the c2a kernel (PAD 10) and the SAGE_HYBRID kernel (ADDR 8, PAD 8)
-    ilp2 = [n for n in ks if re.search(r"ELi2ELi0ELi\d+ELi0EEEvNS_10KernelArgsE$", n)]
+    # <..., ILP=2, PROBE=0, PAD, SYNC=0, FEXTRA=0>: the c2a kernel (PAD 10) and the SAGE_HYBRID kernel (ADDR 8, PAD 8)
+    ilp2 = [n for n in ks if re.search(r"ELi2ELi0ELi\d+ELi0ELi0EEEvNS_10KernelArgsE$", n)]
     assert len(ilp2) == 2 and any("ELi8ELi0ELi0ELb0ELi0ELi2ELi0ELi8E" in n for n in ilp2), ilp2
     for n, r in ks.items():
         if n in ilp2:
