@@ -15,7 +15,12 @@
  *   - output structs are written only on success;
  *   - a wrong checksum is not an error: comparing against the expected value
  *     is the verifier's job;
- *   - sage_last_error() returns a thread-local detail string for the last failure.
+ *   - sage_last_error() returns a thread-local detail string for the last failure;
+ *   - every DEVICE buffer argument (region, per_warp_out, raw_out, counts_out,
+ *     code) is checked with cudaPointerGetAttributes: host memory without a
+ *     device mapping, or another device's allocation, is SAGE_EINVAL rather than
+ *     a fault inside the kernel (managed and mapped pinned memory are accepted;
+ *     the extent of the buffer cannot be checked and is the caller's contract).
  *
  * Ownership: the caller owns `region` (a device pointer, or a host pointer for
  * sage_attest_host) and must keep it alive and unmodified until the call

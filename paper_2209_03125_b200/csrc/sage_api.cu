@@ -155,6 +155,26 @@ int set_device(const sage_ctx* c) {
     return SAGE_OK;
 }
 
+// A buffer the kernel dereferences must be device memory the context's device can
+// read: an unregistered host pointer (or another GPU's allocation) would otherwise
+// fault inside the kernel and leave the CUDA context unusable.  Managed memory and
+// mapped pinned host memory are accepted.
+int check_device_ptr(const sage_ctx* c, const void* p, const char* what) {
+    if (p == nullptr) return SAGE_OK;
+    cudaPointerAttributes at{};
+    const cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();                              // not sticky; clear it
+        return fail(SAGE_EINVAL, "%s is not a CUDA-visible pointer", what);
+    }
+    if (at.type == cudaMemoryTypeUnregistered) return fail(SAGE_EINVAL, "%s is host memory, not device memory", what);
+    if (at.type == cudaMemoryTypeHost && at.devicePointer == nullptr)
+        return fail(SAGE_EINVAL, "%s is pinned host memory without a device mapping", what);
+    if (at.type == cudaMemoryTypeDevice && at.device != c->device)
+        return fail(SAGE_EINVAL, "%s belongs to another device than the context's", what);
+    return SAGE_OK;
+}
+
 // Check the SCS-2 preconditions on (region, bytes, rounds) for P.
 int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t rounds) {
     if (c == nullptr) return fail(SAGE_EINVAL, "null context%s");
@@ -169,7 +189,7 @@ int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t round
     if (reinterpret_cast<uintptr_t>(region) % align != 0)
         return fail(SAGE_EINVAL, "region must be 16-byte aligned (32-byte for P=8)%s");
     if (rounds > 0xFFFFFFFFull) return fail(SAGE_EINVAL, "rounds must be < 2^32%s");
-    return SAGE_OK;
+    return check_device_ptr(c, region, "region");
 }
 
 // SAGE_AUTO: SMEM when the region fits at 2 CTAs/SM, except P = 8, whose
@@ -336,6 +356,8 @@ int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     int rc = validate(ctx, region, region_bytes, rounds);
     if (rc) return rc;
     if (out == nullptr) return fail(SAGE_EINVAL, "out is null%s");
+    rc = check_device_ptr(ctx, per_warp_out, "per_warp_out");
+    if (rc) return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
     sage_result tmp;
     rc = attest_device(ctx, nonce, region, region_bytes, rounds, per_warp_out, &tmp, nullptr);
@@ -349,6 +371,8 @@ int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     int rc = validate(ctx, region, region_bytes, rounds);
     if (rc) return rc;
     if (raw_out == nullptr) return fail(SAGE_EINVAL, "raw_out is null%s");
+    if ((rc = check_device_ptr(ctx, raw_out, "raw_out")) || (rc = check_device_ptr(ctx, per_warp_out, "per_warp_out")))
+        return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
     rc = set_device(ctx);
     if (rc) return rc;
@@ -360,6 +384,8 @@ int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size
     int rc = validate(ctx, region, region_bytes, rounds);
     if (rc) return rc;
     if (counts_out == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    rc = check_device_ptr(ctx, counts_out, "counts_out");
+    if (rc) return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
     rc = set_device(ctx);
     if (rc) return rc;
@@ -376,6 +402,10 @@ int sage_kernel_hash(sage_ctx* ctx, const uint8_t* r, size_t r_len, const void* 
     if (ctx == nullptr || h_out == nullptr || (r == nullptr && r_len) || (code == nullptr && code_len))
         return fail(SAGE_EINVAL, "null pointer%s");
     if (r_len > static_cast<size_t>(sage::kHashRMax)) return fail(SAGE_EINVAL, "r longer than %s bytes", "128");
+    if (code_len) {
+        const int rc = check_device_ptr(ctx, code, "code");
+        if (rc) return rc;
+    }
     std::lock_guard<std::mutex> lock(ctx->mu);
     int rc = set_device(ctx);
     if (rc) return rc;

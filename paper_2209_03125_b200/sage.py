@@ -92,8 +92,8 @@ def load(path=LIB):
     L.sage_last_error.argtypes = []
     L.sage_last_error.restype = ctypes.c_char_p
     for name in ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
-                 "sage_attest_coverage", "sage_kernel_hash",
-                 "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va", "sage_placement_for", "sage_query"):
+                 "sage_attest_coverage", "sage_kernel_hash", "sage_attest_host", "sage_host_region_va",
+                 "sage_placement_for", "sage_query"):
         getattr(L, name).restype = i
     _lib = L
     return L

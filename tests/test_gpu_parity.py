@@ -270,6 +270,37 @@ def test_argument_errors(dev):
         assert e.value.code == sage.SAGE_EUNSUPPORTED
 
 
+def test_host_pointers_rejected_without_faulting(dev):
+    """A host buffer where the kernel needs device memory is SAGE_EINVAL (checked
+    with cudaPointerGetAttributes), not an illegal-address fault that would leave
+    the CUDA context unusable; the context keeps working afterwards.  Pinned host
+    memory is device-mapped under UVA and is accepted."""
+    buf = np.zeros(4096 + 64, dtype=np.uint8)
+    plain = buf.ctypes.data + (-buf.ctypes.data % 64)          # 64-B aligned, unregistered host memory
+    region = torch.zeros(4096, dtype=torch.uint8, device=dev)
+    with sage.Context(blocks=1, threads=32) as ctx:
+        before = ctx.attest(7, region, 100).checksum
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(7, plain, 100, nbytes=4096)
+        assert e.value.code == sage.SAGE_EINVAL and "host memory" in str(e.value)
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest_async(7, region, 100, plain)
+        assert e.value.code == sage.SAGE_EINVAL
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest_debug(7, region, 100, plain)
+        assert e.value.code == sage.SAGE_EINVAL
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest_coverage(7, region, 100, plain)
+        assert e.value.code == sage.SAGE_EINVAL
+        with pytest.raises(sage.SageError) as e:
+            ctx.kernel_hash(b"r", plain, nbytes=64)
+        assert e.value.code == sage.SAGE_EINVAL
+        pinned = torch.zeros(4096, dtype=torch.uint8).pin_memory()
+        res = ctx.attest(7, pinned, 100)
+        assert res.region_va == pinned.data_ptr()
+        assert ctx.attest(7, region, 100).checksum == before
+
+
 def test_maximum_chunk_count(dev):
     """Nc = 2^32 (the SCS-1 maximum): a 16 GiB P=1 region, mask 0xFFFFFFFF,
     64-bit chunk offsets.  Zero-filled except one marker word per 64 MiB on both
