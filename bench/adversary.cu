@@ -36,30 +36,33 @@
 using Fn = void (*)(const sage::KernelArgs);
 struct K { const char* name; Fn fn; int extra; int every; int ilp = 1; };
 
-// <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA, COUNT, EVERY, ILP, PROBE, PAD>; the
-// honest kernel is the product's c2a kernel (XS 16, UNROLL 16, ADDR 4, ILP 2, PAD 10)
+// <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA, COUNT, EVERY, ILP, PROBE, PAD, SYNC, FEXTRA>;
+// the honest kernel is the product's c2a kernel (XS 16, UNROLL 18, ADDR 4, ILP 2, PAD 7)
 static K kernels[] = {
-    {"honest", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10>, 0, 0, 2},
-    {"+1 instr / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 1, 2, 0, 10>, 1, 1, 2},
-    {"+1 instr / 8 rounds", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 8, 2, 0, 10>, 1, 8, 2},
-    {"+1 instr / 16 rounds", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 16, 2, 0, 10>, 1, 16, 2},
-    {"+1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -1, false, 1, 2, 0, 10>, -1, 1, 2},
-    {"+2 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -2, false, 1, 2, 0, 10>, -2, 1, 2},
+    {"honest", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7>, 0, 0, 2},
+    {"+1 instr / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 1, false, 1, 2, 0, 7>, 1, 1, 2},
+    {"+1 instr / 9 rounds", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 1, false, 9, 2, 0, 7>, 1, 9, 2},
+    {"+1 instr / 18 rounds", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 1, false, 18, 2, 0, 7>, 1, 18, 2},
+    {"+1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, -1, false, 1, 2, 0, 7>, -1, 1, 2},
+    {"+2 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, -2, false, 1, 2, 0, 7>, -2, 1, 2},
     // other implementations of the same function an adversary could switch to:
     // the ILP 1 kernel (2 CTAs x 1024 threads per SM, 32 registers; the previous
     // product) and the ILP 2 kernel without the register reservation (56 registers)
     {"ILP1 (2 CTAs/SM)", sage::sage_checksum_kernel<1, true, false, 16, 32, 4, 0, 0>, 0, 0, 1},
     {"ILP1 +1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 32, 4, 0, -1, false, 1>, -1, 1, 1},
+    {"ILP2 U16 PAD10 (previous product)", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10>, 0, 0, 2},
+    {"ILP2 U18 unpadded", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2>, 0, 0, 2},
+    {"ILP2 U18 unpadded +1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, -1, false, 1, 2>, -1, 1, 2},
     {"ILP2 unpadded", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2>, 0, 0, 2},
     {"ILP2 unpadded +1 IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, -1, false, 1, 2>, -1, 1, 2},
     {"ILP2 unpadded +1 instr / 16", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 1, false, 16, 2>, 1, 16, 2},
     // the adversary's own work in the issue slots the checksum leaves idle: a chain
     // independent of the checksum state, FP32 FFMA (FEXTRA > 0) or integer IMAD (< 0)
-    {"+1 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 1>, 0, 1, 2},
-    {"+2 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 2>, 0, 1, 2},
-    {"+4 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 4>, 0, 1, 2},
-    {"+8 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, 8>, 0, 1, 2},
-    {"+1 indep IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 16, 4, 0, 0, false, 0, 2, 0, 10, 0, -1>, 0, 1, 2},
+    {"+1 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7, 0, 1>, 0, 1, 2},
+    {"+2 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7, 0, 2>, 0, 1, 2},
+    {"+4 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7, 0, 4>, 0, 1, 2},
+    {"+8 indep FFMA / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7, 0, 8>, 0, 1, 2},
+    {"+1 indep IMAD / round", sage::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7, 0, -1>, 0, 1, 2},
 };
 
 static uint64_t now_ns() {

@@ -55,8 +55,57 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 #define VARY(U, SY) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD10 SYNC" #SY, \
                   sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, 0, false, 0, 2, 0, 10, SY>, 1, true, false, 2}
 
+#define VARZ(XS, U, A, PAD) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD, \
+                  sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
+
 static V variants[] = {
-    VARY(16, 0), VARY(16, 1), VARY(16, 4), VARY(16, 16), VARY(16, 64), VARY(16, 256), VARY(16, 0),
+    VARH8(2, 196608, 8),
+    VARH8(1, 196608, 0),
+    VARH8(1, 196608, 2),
+    VARH8(1, 196608, 4),
+    VARH8(1, 196608, 5),
+    VARH8(1, 196608, 6),
+    VARH8(1, 196608, 7),
+    VARH8(1, 196608, 8),
+    VARH8(1, 196608, 9),
+    VARH8(1, 196608, 10),
+    VARH8(2, 196608, 0),
+    VARH8(2, 196608, 2),
+    VARH8(2, 196608, 4),
+    VARH8(2, 196608, 5),
+    VARH8(2, 196608, 6),
+    VARH8(2, 196608, 7),
+    VARH8(2, 196608, 8),
+    VARH8(2, 196608, 9),
+    VARH8(2, 196608, 10),
+    VARH8(3, 196608, 0),
+    VARH8(3, 196608, 2),
+    VARH8(3, 196608, 4),
+    VARH8(3, 196608, 5),
+    VARH8(3, 196608, 6),
+    VARH8(3, 196608, 7),
+    VARH8(3, 196608, 8),
+    VARH8(3, 196608, 9),
+    VARH8(3, 196608, 10),
+    VARH8(4, 196608, 0),
+    VARH8(4, 196608, 2),
+    VARH8(4, 196608, 4),
+    VARH8(4, 196608, 5),
+    VARH8(4, 196608, 6),
+    VARH8(4, 196608, 7),
+    VARH8(4, 196608, 8),
+    VARH8(4, 196608, 9),
+    VARH8(4, 196608, 10),
+    VARH8(6, 196608, 0),
+    VARH8(6, 196608, 2),
+    VARH8(6, 196608, 4),
+    VARH8(6, 196608, 5),
+    VARH8(6, 196608, 6),
+    VARH8(6, 196608, 7),
+    VARH8(6, 196608, 8),
+    VARH8(6, 196608, 9),
+    VARH8(6, 196608, 10),
+    VARH8(2, 196608, 8),
 };
 
 int main(int argc, char** argv) {

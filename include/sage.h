@@ -95,7 +95,8 @@ typedef struct {
     uint32_t blocks, threads, pick_words, placement;
     uint32_t ctas_per_sm_smem; /* resident CTAs/SM of the SMEM kernel with a 64 KiB region */
     uint32_t ctas_per_sm_global;
-    uint32_t regs_per_thread;  /* of the P-specific SMEM kernel */
+    uint32_t regs_per_thread;  /* of the P-specific SMEM kernel, as compiled (allocated per warp in
+                                  units of 256, i.e. rounded up to a multiple of 8 per thread) */
     uint64_t smem_region_max;  /* largest region (bytes) SAGE_AUTO stages into SMEM: 64 KiB,
                                   128 KiB at the ILP-2 geometry (see SAGE_AUTO) */
     uint32_t ilp_smem;         /* lane states per thread of that SMEM kernel (1 or 2) */

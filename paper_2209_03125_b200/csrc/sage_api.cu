@@ -82,11 +82,14 @@ template <> struct Unroll<8> { static constexpr int smem = 1, smem_straddle = 1,
 // c2a geometry (P = 1, SMEM, non-straddling, 1024-thread blocks, even block count):
 // two logical lane states per hardware thread (ILP 2), one CTA of 1024 threads per SM,
 // with PAD registers reserved so the CTA allocates the whole 64 K register file
-// (64 registers x 1024 threads) and no other kernel can become resident beside it
-// (P:343-344).  Measured 54.87 vs 55.33 ms per c2a attestation, and it is the
-// fastest implementation of SCS-2 found: an adversary that
-// switched to it would otherwise gain ~0.8% of slack for injected work (section 11).
-constexpr int kIlpSmem = 2, kIlpPad = 10, kIlpUnroll = 16;
+// (62 registers, allocated per warp in units of 256 = 8 per thread -> 64 x 1024) and
+// no other kernel can become resident beside it.  UNROLL and PAD steer
+// ptxas' schedule, which moves the attestation time by up to 6%: a search over
+// 250 (UNROLL, PAD, XS, ADDR) schedules (profiles/r01/variants/ilp2_grid*.jsonl)
+// found 18 / 7 fastest, 53.76-53.94 vs 54.67-54.87 ms for the previous 16 / 10 on
+// three boxes.  It is the fastest implementation of SCS-2 found (DESIGN.md
+// section 8): the verifier's margin is the gap to the fastest form (section 11).
+constexpr int kIlpSmem = 2, kIlpPad = 7, kIlpUnroll = 18;
 
 uint32_t ilp_for(uint32_t P, bool smem, bool straddle, uint32_t blocks, uint32_t threads) {
     return (P == 1 && smem && !straddle && threads == 1024 && blocks % kIlpSmem == 0) ? kIlpSmem : 1;

@@ -2,7 +2,7 @@
 //
 // One launch = one attestation (SAGE section 5.2.2).  Every logical
 // thread of a full-occupancy grid (2048 per SM: 2 CTAs x 1024 threads at 32
-// registers, or -- the c2a kernel -- 1 CTA x 1024 threads x 2 lane states at 64
+// registers, or -- the c2a kernel -- 1 CTA x 1024 threads x 2 lane states at 64 allocated
 // registers; the B200 analogue of P:612-613) seeds its state from the nonce, runs R rounds of
 // SCS-2 entirely in registers, and the folded states are
 // reduced warp (shuffle) -> block (shared memory) -> grid (one 64-bit atomic
@@ -443,7 +443,7 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
-//            CTA x 1024 threads per SM at 64 registers -- the same register file
+//            CTA x 1024 threads per SM at 57-64 registers (64 allocated) -- the same register file
 //            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
           bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0, int SYNC = 0, int FEXTRA = 0>

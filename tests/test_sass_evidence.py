@@ -74,17 +74,18 @@ def test_registers_allow_two_ctas_of_1024(res_usage):
     assert len(ilp2) == 2 and any("ELi8ELi0ELi0ELb0ELi0ELi2ELi0ELi8E" in n for n in ilp2), ilp2
     for n, r in ks.items():
         if n in ilp2:
-            # one CTA of 1024 threads per SM must allocate the whole 64 K register file
-            assert r == 64, (n, r)
+            # one CTA of 1024 threads per SM must allocate the whole 64 K register file:
+            # registers are allocated per warp in units of 256, i.e. 8 per thread
+            assert 56 < r <= 64 and -(-r // 8) * 8 == 64, (n, r)
         else:
             assert r <= 32, (n, r)
 
 
-@pytest.mark.parametrize("name,rounds", [("ILi1ELb1ELb0ELi16ELi16ELi4ELi0ELi0ELb0ELi0ELi2ELi0ELi10E", 32),
+@pytest.mark.parametrize("name,rounds", [("ILi1ELb1ELb0ELi16ELi18ELi4ELi0ELi0ELb0ELi0ELi2ELi0ELi7E", 36),
                                          ("ILi1ELb1ELb0ELi16ELi32ELi4E", 32)])
 def test_c2a_kernel_op_mix(name, rounds):
     """The c2a product kernels (P=1, SMEM, non-straddling, XS=16, ADDR=4; ILP=2
-    with 16 unrolled rounds of two lane states, and the ILP=1 fallback with 32):
+    with 18 unrolled rounds of two lane states, and the ILP=1 fallback with 32):
     per logical round at most 30 ALU-pipe and 26 FMA-pipe instructions (one of them
     the IMAD.WIDE of x*M64), one LDS and one SHFL.IDX -- the minimum ALU count
     for SCS-2's shift/xor/rotate steps (DESIGN.md sections 7-8)."""
