@@ -163,6 +163,12 @@ int main(int argc, char** argv) {
         std::sort(csrt.begin(), csrt.end());
         const double rthr = csrt[size_t(0.99 * (csrt.size() - 1))];
         const double qthr = csrt[size_t(0.95 * (csrt.size() - 1))];   // restart policy threshold
+        // robust relative rule (verifier.calibrate_robust): median * (1 + max(5e-3, 6 * 1.4826 * MAD / median))
+        const double cmed = csrt[csrt.size() / 2];
+        std::vector<double> cdev;
+        for (double x : cal) cdev.push_back(std::fabs(x - cmed));
+        std::sort(cdev.begin(), cdev.end());
+        const double bthr = cmed * (1.0 + std::max(5e-3, 6.0 * 1.4826 * cdev[cdev.size() / 2] / cmed));
         auto frac_above = [](const std::vector<double>& xs, double th) {
             size_t c = 0;
             for (double x : xs) c += x > th;
@@ -173,11 +179,12 @@ int main(int argc, char** argv) {
                "\"detected_tmin_gt_threshold\": %s, \"honest_rejected_frac\": %.3f, \"adversary_rejected_frac\": %.3f, "
                "\"p99_threshold_s\": %.6f, \"p99_honest_rejected_frac\": %.3f, \"p99_adversary_rejected_frac\": %.3f, "
                "\"p95_threshold_s\": %.6f, \"p95_honest_reject_per_try\": %.3f, \"p95_adversary_accept_per_try\": %.3f, "
-               "\"same_checksum\": %s}\n",
+               "\"robust_threshold_s\": %.6f, \"robust_honest_reject_per_try\": %.3f, "
+               "\"robust_adversary_rejected_frac\": %.3f, \"same_checksum\": %s}\n",
                kernels[p[1]].name, kernels[p[0]].name, rounds, cm, cv, thr, as.mn, as.med, as.med / hs.med - 1.0,
                as.mn > thr ? "true" : "false", frac_above(held, thr), frac_above(as.t, thr), rthr,
                frac_above(held, rthr), frac_above(as.t, rthr), qthr, frac_above(held, qthr), 1.0 - frac_above(as.t, qthr),
-               hs.cs == as.cs ? "true" : "false");
+               bthr, frac_above(held, bthr), frac_above(as.t, bthr), hs.cs == as.cs ? "true" : "false");
     }
     return 0;
 }

@@ -76,6 +76,46 @@ class QuantileTimingModel:
         return self.quantile
 
 
+def calibrate_robust(samples, k=6.0, min_margin=5e-3, min_runs=30):
+    """Robust relative timing model: threshold = median * (1 + margin), margin =
+    max(min_margin, k * sigma_r / median) with sigma_r = 1.4826 * MAD, the
+    normal-consistent scale of the main mode.  On B200 the run-time distribution
+    is a tight main mode plus a rare slow mode ~3% above it,
+    so the paper's mean + 2.5 sigma is inflated by the slow runs and a
+    calibrated quantile moves with small drifts; median and MAD ignore both.  Slow
+    honest runs exceed the threshold and are handled by the paper's restart
+    (verify_with_restarts).  The 0.5% floor covers the main mode's width
+    and drift at every measured round count (config 4: held-out false positives
+    per try 0-3%, all of them slow-mode runs at R = 10^5) and stays below the
+    smallest measured adversary slowdown (1.0%)."""
+    xs = [float(s) for s in samples]
+    if len(xs) < min_runs:
+        raise ValueError("calibration needs >= %d runs, got %d" % (min_runs, len(xs)))
+    if k <= 0 or min_margin < 0:
+        raise ValueError("need k > 0 and min_margin >= 0")
+    med = percentile(xs, 50.0)
+    mad = percentile([abs(x - med) for x in xs], 50.0)
+    sigma_r = 1.4826 * mad
+    margin = max(min_margin, k * sigma_r / med)
+    base = calibrate(xs, min_runs=min_runs)
+    return RobustTimingModel(t_avg=base.t_avg, sigma=base.sigma, runs=base.runs, median=med, sigma_r=sigma_r,
+                             margin=margin)
+
+
+@dataclass(frozen=True)
+class RobustTimingModel:
+    t_avg: float
+    sigma: float
+    runs: int
+    median: float
+    sigma_r: float
+    margin: float
+
+    @property
+    def threshold(self):
+        return self.median * (1.0 + self.margin)
+
+
 class NonceLedger:
     """Tracks nonces already used in a session."""
 

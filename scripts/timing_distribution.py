@@ -82,6 +82,10 @@ def run(rounds_list, counts, samples_per_r, out):
                 quantile_fp["q%.2f" % q] = {"threshold": qm.threshold,
                                             "false_positive_rate_second_half":
                                                 sum(1 for x in el[half:] if x > qm.threshold) / max(1, len(el) - half)}
+            rm = verifier.calibrate_robust(el[:half], min_runs=min(30, half))   # median/MAD relative rule
+            robust = {"threshold": rm.threshold, "margin": rm.margin,
+                      "false_positive_rate_second_half": sum(1 for x in el[half:] if x > rm.threshold) /
+                      max(1, len(el) - half)}
             skew, kurt = moments(el)
             entry = {"rounds": R, "n_attest": len(el), "wall_s": time.time() - t_start,
                      "elapsed_s": {"p50": verifier.percentile(el, 50), "p99": verifier.percentile(el, 99),
@@ -94,7 +98,7 @@ def run(rounds_list, counts, samples_per_r, out):
                      "calibrated_on_first_half": {"t_avg": model.t_avg, "sigma": model.sigma,
                                                   "threshold": model.threshold},
                      "false_positive_rate_second_half": fp, "normal_tail_2p5": verifier.normal_tail(2.5),
-                     "quantile_rule": quantile_fp,
+                     "quantile_rule": quantile_fp, "robust_rule": robust,
                      "thread_rounds_per_s_p50": n * R / verifier.percentile(el, 50),
                      "sum_of_partials_ok": sum_ok, "samples": samples,
                      "elapsed_ns_all": [int(round(x * 1e9)) for x in el]}

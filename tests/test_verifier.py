@@ -112,3 +112,43 @@ def test_verify_with_restarts():
     seq = iter([(4, 6, 0.9, 5), (5, 5, 0.9, 5)])
     v, k = V.verify_with_restarts(lambda: next(seq), m)
     assert not v.accepted and v.reason == "checksum_mismatch" and k == 1
+
+
+def test_robust_calibration_closed_forms():
+    """calibrate_robust: median / MAD by hand on a small set, the margin floor, and
+    the normal-consistency constant (1.4826 * MAD estimates sigma for normal data)."""
+    xs = [10.0, 10.1, 9.9, 10.2, 9.8] * 6 + [13.0]           # 31 runs, one slow outlier
+    m = V.calibrate_robust(xs, k=2.0, min_margin=0.0)
+    assert m.median == 10.0
+    assert m.sigma_r == pytest.approx(1.4826 * 0.1)             # |x - 10| medians to 0.1
+    assert m.threshold == pytest.approx(10.0 * (1 + 2.0 * 1.4826 * 0.1 / 10.0))
+    assert m.t_avg > m.median                                   # the mean is pulled up by the outlier
+    assert V.calibrate_robust([5.0] * 30, min_margin=1e-3).threshold == pytest.approx(5.005)
+    rnd = random.Random(7)
+    big = [rnd.gauss(1.0, 0.01) for _ in range(20000)]
+    assert V.calibrate_robust(big, k=1.0, min_margin=0.0).sigma_r == pytest.approx(0.01, rel=0.03)
+    with pytest.raises(ValueError):
+        V.calibrate_robust(xs[:10])
+    with pytest.raises(ValueError):
+        V.calibrate_robust(xs, k=0)
+
+
+def test_robust_rule_ignores_the_slow_mode():
+    """A tight main mode plus a 2% slow mode 3% above it (the B200 distribution,
+    DESIGN.md section 11): the paper's mean + 2.5 sigma threshold is inflated past
+    a +0.8% adversary, the robust threshold is not, and honest slow runs are
+    resolved by the paper's restart."""
+    rnd = random.Random(3)
+    def honest():
+        return rnd.gauss(1.0, 0.0002) * (1.03 if rnd.random() < 0.02 else 1.0)
+    cal = [honest() for _ in range(500)]
+    paper, robust = V.calibrate(cal), V.calibrate_robust(cal)
+    adversary = [rnd.gauss(1.008, 0.0002) for _ in range(200)]     # +0.8%
+    assert sum(t > robust.threshold for t in adversary) == len(adversary)
+    assert sum(t > paper.threshold for t in adversary) < len(adversary) // 2
+    led = V.NonceLedger()
+    n = iter(range(10 ** 6))
+    def attempt():
+        return next(n), 1, honest(), 1
+    outcomes = [V.verify_with_restarts(attempt, robust, max_tries=3, ledger=led)[0].accepted for _ in range(300)]
+    assert all(outcomes)
