@@ -3,8 +3,10 @@
 The verifier accepts an attestation iff the checksum is correct AND it came
 back within the expected time.  The time threshold is
 T_avg + 2.5 sigma over calibration runs (Table 1 row
-"T_avg + 2.5 sigma").  Rejection is a verdict, not an error; on a
-rejection the session restarts with a fresh challenge.
+"T_avg + 2.5 sigma"); calibrate_quantile and
+calibrate_robust (median/MAD, for B200's non-normal run times) are the
+alternatives measured in DESIGN.md section 11.  Rejection is a verdict, not an
+error; on a rejection the session restarts with a fresh challenge.
 
 This is plain host arithmetic over measured numbers; the checksum itself is
 computed only by the CUDA kernel behind libsage.so.
