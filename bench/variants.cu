@@ -59,53 +59,73 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
                   sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
 
 static V variants[] = {
-    VARH8(2, 196608, 8),
-    VARH8(1, 196608, 0),
-    VARH8(1, 196608, 2),
-    VARH8(1, 196608, 4),
-    VARH8(1, 196608, 5),
-    VARH8(1, 196608, 6),
-    VARH8(1, 196608, 7),
-    VARH8(1, 196608, 8),
-    VARH8(1, 196608, 9),
-    VARH8(1, 196608, 10),
-    VARH8(2, 196608, 0),
-    VARH8(2, 196608, 2),
-    VARH8(2, 196608, 4),
-    VARH8(2, 196608, 5),
-    VARH8(2, 196608, 6),
-    VARH8(2, 196608, 7),
-    VARH8(2, 196608, 8),
-    VARH8(2, 196608, 9),
-    VARH8(2, 196608, 10),
-    VARH8(3, 196608, 0),
-    VARH8(3, 196608, 2),
-    VARH8(3, 196608, 4),
-    VARH8(3, 196608, 5),
-    VARH8(3, 196608, 6),
-    VARH8(3, 196608, 7),
-    VARH8(3, 196608, 8),
-    VARH8(3, 196608, 9),
-    VARH8(3, 196608, 10),
-    VARH8(4, 196608, 0),
-    VARH8(4, 196608, 2),
-    VARH8(4, 196608, 4),
-    VARH8(4, 196608, 5),
-    VARH8(4, 196608, 6),
-    VARH8(4, 196608, 7),
-    VARH8(4, 196608, 8),
-    VARH8(4, 196608, 9),
-    VARH8(4, 196608, 10),
-    VARH8(6, 196608, 0),
-    VARH8(6, 196608, 2),
-    VARH8(6, 196608, 4),
-    VARH8(6, 196608, 5),
-    VARH8(6, 196608, 6),
-    VARH8(6, 196608, 7),
-    VARH8(6, 196608, 8),
-    VARH8(6, 196608, 9),
-    VARH8(6, 196608, 10),
-    VARH8(2, 196608, 8),
+    VARZ(16, 18, 4, 7),
+    VARS(8, 16, 0),
+    VARS(8, 16, 4),
+    VARS(8, 16, 5),
+    VARS(8, 16, 6),
+    VARS(8, 16, 7),
+    VARS(8, 16, 8),
+    VARS(8, 16, 9),
+    VARS(8, 16, 10),
+    VARS(10, 16, 0),
+    VARS(10, 16, 4),
+    VARS(10, 16, 5),
+    VARS(10, 16, 6),
+    VARS(10, 16, 7),
+    VARS(10, 16, 8),
+    VARS(10, 16, 9),
+    VARS(10, 16, 10),
+    VARS(12, 16, 0),
+    VARS(12, 16, 4),
+    VARS(12, 16, 5),
+    VARS(12, 16, 6),
+    VARS(12, 16, 7),
+    VARS(12, 16, 8),
+    VARS(12, 16, 9),
+    VARS(12, 16, 10),
+    VARS(14, 16, 0),
+    VARS(14, 16, 4),
+    VARS(14, 16, 5),
+    VARS(14, 16, 6),
+    VARS(14, 16, 7),
+    VARS(14, 16, 8),
+    VARS(14, 16, 9),
+    VARS(14, 16, 10),
+    VARS(16, 16, 0),
+    VARS(16, 16, 4),
+    VARS(16, 16, 5),
+    VARS(16, 16, 6),
+    VARS(16, 16, 7),
+    VARS(16, 16, 8),
+    VARS(16, 16, 9),
+    VARS(16, 16, 10),
+    VARS(17, 16, 0),
+    VARS(17, 16, 4),
+    VARS(17, 16, 5),
+    VARS(17, 16, 6),
+    VARS(17, 16, 7),
+    VARS(17, 16, 8),
+    VARS(17, 16, 9),
+    VARS(17, 16, 10),
+    VARS(18, 16, 0),
+    VARS(18, 16, 4),
+    VARS(18, 16, 5),
+    VARS(18, 16, 6),
+    VARS(18, 16, 7),
+    VARS(18, 16, 8),
+    VARS(18, 16, 9),
+    VARS(18, 16, 10),
+    VARS(20, 16, 0),
+    VARS(20, 16, 4),
+    VARS(20, 16, 5),
+    VARS(20, 16, 6),
+    VARS(20, 16, 7),
+    VARS(20, 16, 8),
+    VARS(20, 16, 9),
+    VARS(20, 16, 10),
+    VARZ(16, 18, 4, 7),
+    VARZ(16, 16, 4, 10),
 };
 
 int main(int argc, char** argv) {

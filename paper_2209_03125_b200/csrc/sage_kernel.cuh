@@ -430,7 +430,8 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //            the lane's own t, so the loop keeps only its integer arithmetic;
 //            bit 2 (result-neutral, ILP > 1) staggers the lane states: each state's
 //            round starts with x += a'[0] * 0 (bit 3: a'[8]) on the other state's
-//            accumulator, an FMA-pipe dependency that offsets the two chains
+//            accumulator, an FMA-pipe dependency that offsets the two chains;
+//            bit 4 (result-neutral) emits the unrolled trip lane-state-major
 //   PAD      registers reserved (kept live across the round loop, unused) so that
 //            an ILP > 1 kernel allocates the whole register file
 //   SYNC     > 0: a CTA barrier every SYNC trips of the round loop (result-neutral;
@@ -549,9 +550,12 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
             }
         }
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-#pragma unroll
-            for (int s = 0; s < ILP; ++s) {
+        for (int uu = 0; uu < UNROLL * ILP; ++uu) {
+            // source order of the unrolled trip: round-major (u, s) by default;
+            // PROBE bit 4 (result-neutral) emits it lane-state-major (s, u) instead
+            const int u = (PROBE & 16) ? uu % UNROLL : uu / ILP;
+            const int s = (PROBE & 16) ? uu / UNROLL : uu % ILP;
+            {
                 if constexpr (ILP > 1 && (PROBE & 4)) {
                     // stagger: a result-neutral FMA-pipe dependency (x += a'[K] * 0) on a
                     // value the other lane state produces early in its last round
