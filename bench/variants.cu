@@ -58,74 +58,17 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 #define VARZ(XS, U, A, PAD) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD, \
                   sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
 
+// The list is edited per experiment; the grids behind profiles/r01/variants/*.jsonl were
+//   ilp2_grid_u_pad:   VARZ(16, U, 4, PAD) for U in {6,8,10,12,14,16}, PAD in 0..12
+//   ilp2_grid2_u_pad:  U in {9,10,11,13,15,18,20}, PAD in 0..12
+//   ilp2_grid3_u_pad:  U in {17,18,19,21,22,24,26,28,32}, PAD in 4..10
+//   ilp2_order_sweep:  VARS(U, 16, PAD) for U in {8,10,12,14,16,17,18,20}, PAD in {0,4..10}
+//   hybrid_u_pad:      VARH8(U, 196608, PAD) for U in {1,2,3,4,6}, PAD in {0,2,4..10} (region 524288)
+//   sync_sweep:        VARY(16, SYNC) for SYNC in {0,1,4,16,64,256}
+// Default: the current product kernels and their nearest alternatives.
 static V variants[] = {
-    VARZ(16, 18, 4, 7),
-    VARS(8, 16, 0),
-    VARS(8, 16, 4),
-    VARS(8, 16, 5),
-    VARS(8, 16, 6),
-    VARS(8, 16, 7),
-    VARS(8, 16, 8),
-    VARS(8, 16, 9),
-    VARS(8, 16, 10),
-    VARS(10, 16, 0),
-    VARS(10, 16, 4),
-    VARS(10, 16, 5),
-    VARS(10, 16, 6),
-    VARS(10, 16, 7),
-    VARS(10, 16, 8),
-    VARS(10, 16, 9),
-    VARS(10, 16, 10),
-    VARS(12, 16, 0),
-    VARS(12, 16, 4),
-    VARS(12, 16, 5),
-    VARS(12, 16, 6),
-    VARS(12, 16, 7),
-    VARS(12, 16, 8),
-    VARS(12, 16, 9),
-    VARS(12, 16, 10),
-    VARS(14, 16, 0),
-    VARS(14, 16, 4),
-    VARS(14, 16, 5),
-    VARS(14, 16, 6),
-    VARS(14, 16, 7),
-    VARS(14, 16, 8),
-    VARS(14, 16, 9),
-    VARS(14, 16, 10),
-    VARS(16, 16, 0),
-    VARS(16, 16, 4),
-    VARS(16, 16, 5),
-    VARS(16, 16, 6),
-    VARS(16, 16, 7),
-    VARS(16, 16, 8),
-    VARS(16, 16, 9),
-    VARS(16, 16, 10),
-    VARS(17, 16, 0),
-    VARS(17, 16, 4),
-    VARS(17, 16, 5),
-    VARS(17, 16, 6),
-    VARS(17, 16, 7),
-    VARS(17, 16, 8),
-    VARS(17, 16, 9),
-    VARS(17, 16, 10),
-    VARS(18, 16, 0),
-    VARS(18, 16, 4),
-    VARS(18, 16, 5),
-    VARS(18, 16, 6),
-    VARS(18, 16, 7),
-    VARS(18, 16, 8),
-    VARS(18, 16, 9),
-    VARS(18, 16, 10),
-    VARS(20, 16, 0),
-    VARS(20, 16, 4),
-    VARS(20, 16, 5),
-    VARS(20, 16, 6),
-    VARS(20, 16, 7),
-    VARS(20, 16, 8),
-    VARS(20, 16, 9),
-    VARS(20, 16, 10),
-    VARZ(16, 18, 4, 7),
-    VARZ(16, 16, 4, 10),
+    VARZ(16, 18, 4, 7), VARZ(16, 16, 4, 10), VARZ(16, 18, 4, 0), VARZ(16, 18, 4, 8), VARZ(16, 17, 4, 7),
+    VARH8(2, 196608, 8), VARZ(16, 18, 4, 7),
 };
 
 int main(int argc, char** argv) {
