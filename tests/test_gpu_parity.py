@@ -248,7 +248,7 @@ def test_ilp2_and_ilp1_kernels_agree(dev):
 def test_argument_errors(dev):
     region = torch.zeros(1 << 20, dtype=torch.uint8, device=dev)
     with sage.Context(blocks=1, threads=32) as ctx:
-        for nbytes in (12, 24, 3 * 4096):
+        for nbytes in (0, 12, 24, 3 * 4096):             # empty, not 4P*2^k
             with pytest.raises(sage.SageError) as e:
                 ctx.attest(0, region, 1, nbytes=nbytes)
             assert e.value.code == sage.SAGE_EINVAL
