@@ -6,6 +6,7 @@ include/sage.h (libsage.so, built in-tree by paper_2209_03125_b200.build);
 library is missing.
 """
 from . import inputs, verifier                      # noqa: F401
-from .sage import (SAGE_AUTO, SAGE_GLOBAL, SAGE_SMEM, Context, SageError,  # noqa: F401
-                   attest, attest_async, attest_debug, attest_host, checksum_destroy, checksum_init,
-                   decode_raw, host_region_va, launch_count, load, placement_for, query)
+from .sage import (SAGE_AUTO, SAGE_GLOBAL, SAGE_HYBRID, SAGE_SMEM, Context, SageError,  # noqa: F401
+                   attest, attest_async, attest_coverage, attest_debug, attest_host, checksum_destroy,
+                   checksum_init, decode_raw, host_region_va, kernel_hash, launch_count, load, placement_for,
+                   query)
