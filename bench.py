@@ -201,7 +201,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2209_03125_b200 import build, replicas, sage
+    from paper_2209_03125_b200 import build, replicas, sage, verifier
     from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region
 
     ws, rank, local = dist_env()
@@ -345,7 +345,9 @@ def run_ours(args):
                 "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(kern_s), "max": 1e3 * max(kern_s)},
                 "attest_ms": {"p50": statistics.median(att), "p99": _pct(att, 99), "mean": statistics.mean(att),
                               "sigma": statistics.pstdev(att), "threshold_2p5sigma":
-                              statistics.mean(att) + 2.5 * statistics.pstdev(att), "n": len(att)},
+                              statistics.mean(att) + 2.5 * statistics.pstdev(att),
+                              "threshold_robust": (verifier.calibrate_robust(att, min_runs=1).threshold
+                                                   if len(att) >= 3 else None), "n": len(att)},
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
         if clocks.get("power_w_median"):
             line["energy_j_per_attestation"] = clocks["power_w_median"] * mean_k
