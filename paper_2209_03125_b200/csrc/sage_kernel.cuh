@@ -197,6 +197,9 @@ struct KernelArgs {
     uint32_t* counts;         // COUNT variant only: per-chunk read counters (inclusion experiment)
     uint64_t* cta_trace;      // optional: per CTA {smid, start ns, end ns, clock64 span} (diagnostics)
     uint32_t slice_shift;     // ADDR == 3 (cluster-distributed SMEM): log2 of the bytes each CTA holds
+    uint64_t* progress;       // PROBE bit 5 only: per CTA, %globaltimer every progress_every trips
+    uint32_t progress_every;  //   (progress[blockIdx.x * progress_slots + k]); diagnostics
+    uint32_t progress_slots;
 };
 
 // The region staged in shared memory (SMEM placement): namespace-scope so the
@@ -431,7 +434,8 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //            bit 2 (result-neutral, ILP > 1) staggers the lane states: each state's
 //            round starts with x += a'[0] * 0 (bit 3: a'[8]) on the other state's
 //            accumulator, an FMA-pipe dependency that offsets the two chains;
-//            bit 4 (result-neutral) emits the unrolled trip lane-state-major
+//            bit 4 (result-neutral) emits the unrolled trip lane-state-major;
+//            bit 5 (result-neutral) stamps a per-CTA progress trace (args.progress)
 //   PAD      registers reserved (kept live across the round loop, unused) so that
 //            an ILP > 1 kernel allocates the whole register file
 //   SYNC     > 0: a CTA barrier every SYNC trips of the round loop (result-neutral;
@@ -541,7 +545,17 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
         fadv[s] = static_cast<float>(lane + s);
         iadv[s] = lane + s;
     }
+    [[maybe_unused]] uint32_t trip = 0;
     for (; r < main_end; r += UNROLL) {
+        if constexpr (PROBE & 32) {
+            // progress trace (diagnostics, result-neutral): thread 0 stamps %globaltimer
+            if (threadIdx.x == 0 && trip % args.progress_every == 0) {
+                const uint32_t k = trip / args.progress_every;
+                if (k < args.progress_slots) args.progress[static_cast<uint64_t>(blockIdx.x) * args.progress_slots + k] =
+                    globaltimer();
+            }
+            ++trip;
+        }
         if constexpr (SYNC > 0) {
             // keep the CTA's warps within SYNC trips of each other (result-neutral)
             if (--trips_to_sync == 0) {
