@@ -34,3 +34,24 @@ def test_full_occupancy_full_rounds_every_warp():
     bad = [w for w in range(n // 32) if parts[w] != want[w]]
     assert not bad, bad[:10]
     assert sum(want.values()) & M64 == res.checksum
+
+
+def test_config4_full_result_twenty_nonces():
+    """Config 4's shortest round count (R = 10^4) at full occupancy: the whole
+    checksum of 20 nonces from the bench's nonce stream recomputed by the oracle
+    (every warp; full parity for >= 20 nonces, sampled warps +
+    sum consistency for the rest, which tests/test_c4_samples.py covers)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d = torch.from_numpy(region).to("cuda")
+    R = 10_000
+    ns = nonces(22)[2:]
+    with sage.Context() as ctx:
+        info = ctx.query()
+        n = info.blocks * info.threads
+        got = [ctx.attest(nonce, d, R).checksum for nonce in ns]
+    with oracle.WarpPool(region, len(os.sched_getaffinity(0))) as pool:
+        for nonce, checksum in zip(ns, got):
+            want = pool.warp_sums(nonce, d.data_ptr(), R, range(n // 32), 1)
+            assert sum(want.values()) & M64 == checksum, hex(nonce)
