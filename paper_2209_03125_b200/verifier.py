@@ -118,6 +118,23 @@ class RobustTimingModel:
         return self.median * (1.0 + self.margin)
 
 
+def stall_estimate(samples, floor=1e-3):
+    """The B200 slow mode as fixed-length whole-chip pauses:
+    runs more than `floor` seconds above the median are counted as containing a
+    pause; returns their share, the median excess (the pause length) and the
+    Poisson rate per second of attestation implied by P(>= 1 pause) =
+    1 - exp(-rate * T) with T the median run time."""
+    xs = [float(s) for s in samples]
+    if not xs:
+        raise ValueError("empty")
+    med = percentile(xs, 50.0)
+    excess = [x - med for x in xs if x - med > floor]
+    frac = len(excess) / len(xs)
+    rate = -math.log1p(-frac) / med if 0.0 < frac < 1.0 and med > 0 else (0.0 if frac == 0.0 else math.inf)
+    return {"runs": len(xs), "median_s": med, "paused_runs": len(excess), "paused_frac": frac,
+            "excess_median_s": percentile(excess, 50.0) if excess else None, "rate_per_s": rate}
+
+
 class NonceLedger:
     """Tracks nonces already used in a session."""
 

@@ -99,6 +99,7 @@ def run(rounds_list, counts, samples_per_r, out):
                                                   "threshold": model.threshold},
                      "false_positive_rate_second_half": fp, "normal_tail_2p5": verifier.normal_tail(2.5),
                      "quantile_rule": quantile_fp, "robust_rule": robust,
+                     "stalls": verifier.stall_estimate(el),
                      "thread_rounds_per_s_p50": n * R / verifier.percentile(el, 50),
                      "sum_of_partials_ok": sum_ok, "samples": samples,
                      "elapsed_ns_all": [int(round(x * 1e9)) for x in el]}

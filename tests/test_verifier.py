@@ -152,3 +152,15 @@ def test_robust_rule_ignores_the_slow_mode():
         return next(n), 1, honest(), 1
     outcomes = [V.verify_with_restarts(attempt, robust, max_tries=3, ledger=led)[0].accepted for _ in range(300)]
     assert all(outcomes)
+
+
+def test_stall_estimate_recovers_injected_pauses():
+    """Fixed 1.7 ms pauses injected into a constant main mode: count, share,
+    pause length and the Poisson rate -ln(1 - frac) / T are recovered exactly."""
+    T = 0.054
+    xs = [T] * 975 + [T + 0.0017] * 25
+    est = V.stall_estimate(xs)
+    assert est["paused_runs"] == 25 and est["paused_frac"] == 0.025
+    assert est["excess_median_s"] == pytest.approx(0.0017)
+    assert est["rate_per_s"] == pytest.approx(-math.log(1 - 0.025) / T)
+    assert V.stall_estimate([T] * 10)["rate_per_s"] == 0.0
