@@ -8,7 +8,9 @@
 
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <new>
 
 #include "sage.h"
@@ -213,6 +215,22 @@ uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
     return SAGE_GLOBAL;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is only called when a launch
+// needs more dynamic shared memory than the kernel already allows on that
+// device: setting it on every attestation costs host time between back-to-back
+// launches.  Process-wide, guarded by a mutex (contexts may share kernels).
+int ensure_dyn_smem(int device, KernelFn fn, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> set;
+    std::lock_guard<std::mutex> lock(mu);
+    int& cur = set[{device, reinterpret_cast<const void*>(fn)}];
+    if (bytes <= cur) return SAGE_OK;
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bytes));
+    cur = bytes;
+    return SAGE_OK;
+}
+
 int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
            uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
     uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
@@ -243,8 +261,10 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
         fn = hybrid_kernel();
     }
     const size_t dyn = smem ? bytes : hybrid ? (bytes < kHybridStage ? bytes : kHybridStage) : 0;
-    if (dyn) CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+    if (dyn) {
+        int rc = ensure_dyn_smem(c->device, fn, static_cast<int>(dyn));
+        if (rc) return rc;
+    }
     sage::KernelArgs args{};
     args.region = static_cast<const uint32_t*>(region);
     args.nonce = nonce;
@@ -489,8 +509,8 @@ int sage_query(sage_ctx* ctx, sage_info* out) {
     const uint32_t ilp = ilp_for(ctx->pick_words, true, false, ctx->blocks, ctx->threads);
     info.ilp_smem = ilp;
     KernelFn fs = kernel_for(ctx->pick_words, true, false, ilp), fg = kernel_for(ctx->pick_words, false, true);
-    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fs), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemRegionMax)));
+    rc = ensure_dyn_smem(ctx->device, fs, static_cast<int>(kSmemRegionMax));
+    if (rc) return rc;
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs, static_cast<int>(ctx->threads), kSmemRegionMax));
     info.ctas_per_sm_smem = static_cast<uint32_t>(occ);
