@@ -219,12 +219,13 @@ uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
 // needs more dynamic shared memory than the kernel already allows on that
 // device: setting it on every attestation costs host time between back-to-back
 // launches.  Process-wide, guarded by a mutex (contexts may share kernels).
-int ensure_dyn_smem(int device, KernelFn fn, int bytes) {
+// force = true re-applies the attribute (after a device reset the cache is stale).
+int ensure_dyn_smem(int device, KernelFn fn, int bytes, bool force = false) {
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, int> set;
     std::lock_guard<std::mutex> lock(mu);
     int& cur = set[{device, reinterpret_cast<const void*>(fn)}];
-    if (bytes <= cur) return SAGE_OK;
+    if (bytes <= cur && !force) return SAGE_OK;
     CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bytes));
     cur = bytes;
@@ -276,7 +277,15 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     args.counts = counts;
     sage::fill_tables(args, c->pick_words);
     fn<<<c->blocks / ilp, c->threads, dyn, c->stream>>>(args);
-    CUDA_TRY(cudaGetLastError());
+    cudaError_t le = cudaGetLastError();
+    if (le == cudaErrorInvalidValue && dyn) {
+        // the cached shared-memory limit is stale (e.g. cudaDeviceReset): re-apply it once
+        int rc = ensure_dyn_smem(c->device, fn, static_cast<int>(dyn), true);
+        if (rc) return rc;
+        fn<<<c->blocks / ilp, c->threads, dyn, c->stream>>>(args);
+        le = cudaGetLastError();
+    }
+    if (le != cudaSuccess) return cuda_fail(le, "checksum kernel launch");
     c->launches++;
     if (placement_used) *placement_used = placement;
     if (ilp_used) *ilp_used = ilp;
