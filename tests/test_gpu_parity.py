@@ -529,3 +529,35 @@ def test_paper_buffer_full_occupancy_sampled(dev):
     assert sum(parts) & M64 == res.checksum
     for w in (0, 1, n // 64, n // 32 - 1):
         assert parts[w] == oracle.warp_sum(0xC2C, region, d.data_ptr(), R, w, 1), w
+
+
+def test_no_other_kernel_runs_beside_an_attestation(dev):
+    """Full occupancy leaves no room for another kernel: a tiny kernel
+    launched on a second stream right after the attestation cannot start until
+    the attestation's CTAs leave their SMs, so it finishes only at the end of the
+    attestation; with a half-occupancy grid (control) it runs at once."""
+    region = torch.from_numpy(make_region(8192)).to(dev)
+    side = torch.zeros(1024, device=dev)
+    sa, sb = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    for blocks, threads, full in ((0, 0, True), (148, 512, False)):
+        with sage.Context(blocks=blocks, threads=threads, stream=sa) as ctx:
+            raw = torch.zeros(4, dtype=torch.int64, device=dev)
+            ctx.attest_async(1, region, 200, raw)                       # warm-up
+            torch.cuda.synchronize(dev)
+            raw.zero_()
+            e0, e1, eb = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            with torch.cuda.stream(sa):
+                e0.record(sa)
+                ctx.attest_async(2, region, 20_000, raw)              # ~11 ms at full occupancy
+                e1.record(sa)
+            with torch.cuda.stream(sb):
+                side.add_(1.0)
+                eb.record(sb)
+            torch.cuda.synchronize(dev)
+            t_att, t_side = e0.elapsed_time(e1), e0.elapsed_time(eb)
+            print("co-residency probe: blocks=%d threads=%d attestation %.3f ms, side kernel done at %.3f ms"
+                  % (blocks, threads, t_att, t_side))
+        if full:
+            assert t_side > 0.9 * t_att, (t_side, t_att)
+        else:
+            assert t_side < 0.5 * t_att, (t_side, t_att)
