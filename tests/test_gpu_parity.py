@@ -561,3 +561,19 @@ def test_no_other_kernel_runs_beside_an_attestation(dev):
             assert t_side > 0.9 * t_att, (t_side, t_att)
         else:
             assert t_side < 0.5 * t_att, (t_side, t_att)
+
+
+def test_relocated_copy_gives_a_different_checksum(dev):
+    """The data pointer is folded in every round, so the same bytes
+    attested at another device address (a relocated copy of the verification
+    function) give a different checksum -- each equal to the oracle's at its own VA."""
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d1, _k1 = to_dev(region, dev)
+    d2, _k2 = to_dev(region, dev, align_offset=4096)
+    assert d1.data_ptr() != d2.data_ptr()
+    with sage.Context(blocks=2, threads=64) as ctx:
+        c1 = ctx.attest(C1_NONCE, d1, 500).checksum
+        c2 = ctx.attest(C1_NONCE, d2, 500).checksum
+    assert c1 != c2
+    assert c1 == oracle.attest(C1_NONCE, region, d1.data_ptr(), 500, 2, 64, 1)
+    assert c2 == oracle.attest(C1_NONCE, region, d2.data_ptr(), 500, 2, 64, 1)
