@@ -577,3 +577,28 @@ def test_relocated_copy_gives_a_different_checksum(dev):
     assert c1 != c2
     assert c1 == oracle.attest(C1_NONCE, region, d1.data_ptr(), 500, 2, 64, 1)
     assert c2 == oracle.attest(C1_NONCE, region, d2.data_ptr(), 500, 2, 64, 1)
+
+
+def test_single_bit_flips_change_the_gpu_checksum(dev):
+    """Self-verification: flipping any one bit of the region changes
+    the attestation result; 16 random bits of an 8 KiB region at full occupancy
+    with enough rounds that every word is read (R = 64), each result equal to
+    the oracle's on the flipped bytes."""
+    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    d, _keep = to_dev(region, dev)
+    rng = np.random.default_rng(11)
+    with sage.Context() as ctx:
+        base_cs = ctx.attest(0xF11B, d, 64).checksum
+        info = ctx.query()
+        for bit in rng.integers(0, 8192 * 8, 16):
+            flipped = region.copy()
+            flipped[bit // 8] ^= np.uint8(1 << (bit % 8))
+            d.copy_(torch.from_numpy(flipped))
+            cs = ctx.attest(0xF11B, d, 64).checksum
+            assert cs != base_cs, int(bit)
+            w = int(rng.integers(0, info.blocks * info.threads // 32))
+            pw = torch.zeros(info.blocks * info.threads // 32, dtype=torch.int64, device=dev)
+            ctx.attest_debug(0xF11B, d, 64, pw)
+            assert int(pw[w].item()) & M64 == oracle.warp_sum(0xF11B, flipped, d.data_ptr(), 64, w, 1)
+        d.copy_(torch.from_numpy(region))
+        assert ctx.attest(0xF11B, d, 64).checksum == base_cs
