@@ -70,8 +70,12 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 //   ilp2_xs_sweep:     VARZ(XS, U, 4, PAD) for XS in {17,18,20}, U in {16,17,18}, PAD in {0,5,6,7,8,10}
 // Default: the current product kernels and their nearest alternatives.
 static V variants[] = {
+#ifdef VARIANTS_INC
+#include VARIANTS_INC          // a generated list (scripts/schedule_search.py)
+#else
     VARZ(16, 18, 4, 7), VARZ(16, 16, 4, 10), VARZ(16, 18, 4, 0), VARZ(16, 18, 4, 8), VARZ(16, 17, 4, 7),
     VARH8(2, 196608, 8), VARZ(16, 18, 4, 7),
+#endif
 };
 
 int main(int argc, char** argv) {

@@ -1,0 +1,129 @@
+"""Schedule search for the c2a checksum kernel.
+
+UNROLL and PAD (and the XS / ADDR lowerings) leave SCS-2's arithmetic unchanged
+but change ptxas' register assignment and instruction schedule, which moves the
+attestation time by several percent.  This tool builds bench/variants.cu over
+a grid of those knobs (ILP = 2, 1024-thread CTAs), records each variant's
+register count, and -- with --run, on a B200 -- times every variant `--passes`
+times (3 launches each, best kept), checks they all return the same checksum,
+and prints the ranking.  The verifier's margin is the gap between the product
+and the fastest implementation anyone can build, so the
+search is kept runnable: an attacker can run it too.
+
+    python scripts/schedule_search.py --unroll 16-19 --pad 0-12 --out gpurun_out/search.jsonl --run
+"""
+import argparse
+import json
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "bench", "variants.cu")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def parse_range(spec):
+    """'16-19' -> [16, 17, 18, 19]; '1,4,8' -> [1, 4, 8]; mixed forms allowed."""
+    out = []
+    for part in str(spec).split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            out.extend(range(int(a), int(b) + 1))
+        elif part:
+            out.append(int(part))
+    return out
+
+
+def grid(unrolls, pads, xss, addrs):
+    return [(xs, u, a, p) for xs in xss for u in unrolls for a in addrs for p in pads]
+
+
+def build(points, binary):
+    """Compile bench/variants.cu with the generated list; return {point: registers}."""
+    with tempfile.NamedTemporaryFile("w", suffix=".inc", delete=False) as f:
+        for xs, u, a, p in points:
+            f.write("    VARZ(%d, %d, %d, %d),\n" % (xs, u, a, p))
+        inc = f.name
+    try:
+        subprocess.check_call(["nvcc"] + ARCH + ["-O3", "-lineinfo", "-std=c++17",
+                                                 "-I" + os.path.join(ROOT, "paper_2209_03125_b200", "csrc"),
+                                                 "-I" + os.path.join(ROOT, "include"),
+                                                 '-DVARIANTS_INC="%s"' % inc, "-o", binary, SRC])
+    finally:
+        os.unlink(inc)
+    usage = subprocess.run(["cuobjdump", "-res-usage", binary], capture_output=True, text=True, check=True).stdout
+    regs, name = {}, None
+    for ln in usage.splitlines():
+        m = re.search(r"Function (\S+):", ln)
+        if m:
+            name = m.group(1)
+        m = re.search(r"REG:(\d+)", ln)
+        if m and name:
+            t = re.search(r"kernelILi1ELb1ELb0ELi(\d+)ELi(\d+)ELi(\d+)ELi0ELi0ELb0ELi0ELi2ELi0ELi(\d+)E", name)
+            if t:
+                xs, u, a, p = (int(v) for v in t.groups())
+                regs[(xs, u, a, p)] = int(m.group(1))
+    return regs
+
+
+def run(binary, passes, rounds, nbytes):
+    """Time the variants; returns {variant name: [ms per pass]} and whether, within
+    every pass, all variants returned the same checksum (the region's device VA,
+    which the checksum depends on, may differ between passes)."""
+    times, same = {}, True
+    for _ in range(passes):
+        out = subprocess.run([binary, str(rounds), str(nbytes)], capture_output=True, text=True, check=True).stdout
+        sums = set()
+        for ln in out.splitlines():
+            if ln.startswith("{"):
+                d = json.loads(ln)
+                times.setdefault(d["variant"], []).append(d["ms"])
+                sums.add(d["checksum"])
+        same = same and len(sums) == 1
+    return times, same
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--unroll", default="16-19")
+    ap.add_argument("--pad", default="0-12")
+    ap.add_argument("--xs", default="16")
+    ap.add_argument("--addr", default="4")
+    ap.add_argument("--rounds", type=int, default=100_000)
+    ap.add_argument("--bytes", type=int, default=8192)
+    ap.add_argument("--passes", type=int, default=2)
+    ap.add_argument("--binary", default=os.path.join(ROOT, "bench", "variants_search"))
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--run", action="store_true", help="time the variants (needs a B200)")
+    a = ap.parse_args()
+    points = grid(parse_range(a.unroll), parse_range(a.pad), parse_range(a.xs), parse_range(a.addr))
+    regs = build(points, a.binary)
+    print(json.dumps({"built": len(points), "binary": a.binary}), flush=True)
+    if not a.run:
+        for pt in points:
+            print(json.dumps({"xs": pt[0], "unroll": pt[1], "addr": pt[2], "pad": pt[3], "registers": regs.get(pt)}))
+        return 0
+    times, same = run(a.binary, a.passes, a.rounds, a.bytes)
+    rows = []
+    for pt in points:
+        name = "P1 smem xs%d unroll%d addr%d ILP2 PAD%d" % pt
+        if name in times:
+            r = regs.get(pt)
+            rows.append({"xs": pt[0], "unroll": pt[1], "addr": pt[2], "pad": pt[3], "registers": r,
+                         "full_register_file": r is not None and 56 < r <= 64, "ms": min(times[name]),
+                         "ms_all": times[name]})
+    rows.sort(key=lambda d: d["ms"])
+    lines = [json.dumps(dict(d, same_checksum=same)) for d in rows]
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write("\n".join(lines) + "\n")
+    for ln in lines[:10]:                      # fastest first
+        print(ln)
+    return 0 if same else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
