@@ -86,8 +86,9 @@ template <> struct Unroll<8> { static constexpr int smem = 1, smem_straddle = 1,
 // with PAD registers reserved so the CTA allocates the whole 64 K register file
 // (62 registers, allocated per warp in units of 256 = 8 per thread -> 64 x 1024) and
 // no other kernel can become resident beside it.  UNROLL and PAD steer
-// ptxas' schedule, which moves the attestation time by up to 6%: a search over
-// 250 (UNROLL, PAD, XS, ADDR) schedules (profiles/r01/variants/ilp2_grid*.jsonl)
+// ptxas' schedule, which moves the attestation time by up to 10%: searches over
+// ~700 (UNROLL, PAD, XS, ADDR) schedules (profiles/r01/variants/ilp2_grid*.jsonl,
+// schedule_search_429.jsonl; scripts/schedule_search.py)
 // found 18 / 7 fastest, 53.76-53.94 vs 54.67-54.87 ms for the previous 16 / 10 on
 // three boxes.  It is the fastest implementation of SCS-2 found (DESIGN.md
 // section 8): the verifier's margin is the gap to the fastest form (section 11).
