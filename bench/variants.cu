@@ -68,6 +68,7 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 //   ilp4_grid_u_pad:   VARQ(U, 4, PAD, 512) for U in {2,3,4,6,8}, PAD in {0,8,14..24 step 2}
 //   ilp2_t512_sweep:   VARQ(U, 2, PAD, 512) for U in {16,17,18}, PAD in {0,6,7,8,10}
 //   ilp2_xs_sweep:     VARZ(XS, U, 4, PAD) for XS in {17,18,20}, U in {16,17,18}, PAD in {0,5,6,7,8,10}
+//   hybrid_stage_sweep: VARH8(2, STAGE, 8) for STAGE in 160..212 KiB (region 524288)
 // Default: the current product kernels and their nearest alternatives.
 static V variants[] = {
 #ifdef VARIANTS_INC
