@@ -81,7 +81,7 @@ typedef struct {
     uint64_t device_ns;   /* %globaltimer: last CTA end - first CTA start */
     uint64_t region_va;   /* device VA the region was read from (the `base` of SCS-2) */
     uint32_t placement;   /* SAGE_SMEM, SAGE_GLOBAL or SAGE_HYBRID actually used */
-    uint32_t blocks;      /* grid actually launched */
+    uint32_t blocks;      /* logical grid (blocks x threads logical threads; see ilp) */
     uint32_t threads;     /* block size actually launched */
     uint32_t pick_words;  /* P actually used */
     uint32_t ilp;         /* logical lane states per hardware thread (1 or 2): the launch was
