@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "checksum rounds/s and checksummed GB/s per B200 (1/2/4/8 GPU); p99 attest time"
 UNIT = "thread-rounds/s"
+ATTEST_SAMPLES, ATTEST_BUDGET_S = 200, 15.0   # attest_ms distribution: up to 200 runs / ~15 s
 CPU_SAMPLE_S = 20.0          # cpu_baseline sizing target (the one-warp-per-core calibration pass
                              # overestimates the per-warp cost ~2x, so the timed sample runs ~10 s)
 
@@ -307,11 +308,16 @@ def run_ours(args):
                "l2": "not flushed: each step's H2D copy rewrites the region just before the kernel reads it"}
         ctx_h.close()
 
-    # attestation wall time as the verifier sees it (sage_attest, device region)
+    # attestation wall time as the verifier sees it (sage_attest, device region):
+    # ATTEST_SAMPLES attestations (at least --steps) or ATTEST_BUDGET_S of them,
+    # whichever ends first, so that p99 is more than the maximum of a few runs
     att = []
-    for k in range(args.steps):
+    t_att0 = time.perf_counter()
+    for k in range(max(args.steps, ATTEST_SAMPLES)):
         r = ctx.attest(my_nonces[total + (k % 64)], region, R)
         att.append(r.elapsed_ns / 1e6)
+        if k + 1 >= args.steps and time.perf_counter() - t_att0 > ATTEST_BUDGET_S:
+            break
 
     # per-warp partials of one attestation, for the sampled parity check below
     pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
