@@ -55,6 +55,9 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 #define VARY(U, SY) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD10 SYNC" #SY, \
                   sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, 0, false, 0, 2, 0, 10, SY>, 1, true, false, 2}
 
+#define VARHS(U, PR, PAD) {"P1 hybrid8 unroll" #U " ILP2 stage196608 PROBE" #PR " PAD" #PAD, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 8, 0, 0, false, 0, 2, PR, PAD>, 1, true, false, 2, 0, 196608, PR}
+
 #define VARZ(XS, U, A, PAD) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD, \
                   sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
 
@@ -69,6 +72,7 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 //   ilp2_t512_sweep:   VARQ(U, 2, PAD, 512) for U in {16,17,18}, PAD in {0,6,7,8,10}
 //   ilp2_xs_sweep:     VARZ(XS, U, 4, PAD) for XS in {17,18,20}, U in {16,17,18}, PAD in {0,5,6,7,8,10}
 //   hybrid_stage_sweep: VARH8(2, STAGE, 8) for STAGE in 160..212 KiB (region 524288)
+//   hybrid_stagger:    VARHS(U, PROBE, PAD) for PROBE in {4, 12} (region 524288)
 // Default: the current product kernels and their nearest alternatives.
 static V variants[] = {
 #ifdef VARIANTS_INC
