@@ -22,7 +22,8 @@
 #include <cstdlib>
 #include <vector>
 
-#include "sage_kernel.cuh"
+#include "sage_lab.cuh"
+namespace sage = sage_lab;
 
 #define CK(x)                                                                  \
     do {                                                                       \

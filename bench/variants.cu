@@ -1,5 +1,5 @@
 // variants.cu -- development harness: times lowering variants of the SCS-2
-// kernel (sage_kernel.cuh) at full occupancy on one SMEM/GLOBAL workload and
+// kernel (the lab form, bench/sage_lab.cuh) at full occupancy on one SMEM/GLOBAL workload and
 // checks they all return the same checksum.  Not part of the product path.
 //
 //   ./variants [rounds] [region_bytes]
@@ -10,7 +10,8 @@
 #include <cstring>
 #include <vector>
 
-#include "sage_kernel.cuh"
+#include "sage_lab.cuh"
+namespace sage = sage_lab;
 
 #define CK(x)                                                                  \
     do {                                                                       \
@@ -57,6 +58,16 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 
 #define VARHS(U, PR, PAD) {"P1 hybrid8 unroll" #U " ILP2 stage196608 PROBE" #PR " PAD" #PAD, \
                   sage::sage_checksum_kernel<1, true, false, 16, U, 8, 0, 0, false, 0, 2, PR, PAD>, 1, true, false, 2, 0, 196608, PR}
+
+// round 2: HBM regions with per-pick L2 eviction priority (LD 5/6, PERSIST_BYTES env)
+#define VARGL(P, U, LD) {"P" #P " global xs16 unroll" #U " LD" #LD, \
+                  sage::sage_checksum_kernel<P, false, true, 16, U, 0, LD>, P, false, true}
+// round 2: hybrid over a 2-CTA cluster (ADDR 9), each CTA stages a different ST bytes
+#define VARH9(U, ST, PAD) {"P1 hybrid9 cluster2 unroll" #U " ILP2 stage" #ST " PAD" #PAD, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 9, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2, 2, ST}
+// attacker's schedule search: the c2a kernel + EXTRA injected every EVERY rounds
+#define VARE(U, PAD, EXTRA, EVERY) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD" #PAD " EXTRA" #EXTRA " EVERY" #EVERY, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, EXTRA, false, EVERY, 2, 0, PAD>, 1, true, false, 2}
 
 #define VARZ(XS, U, A, PAD) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD, \
                   sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
@@ -110,6 +121,37 @@ int main(int argc, char** argv) {
     const bool straddles = (reinterpret_cast<uint64_t>(d) >> 32) != ((reinterpret_cast<uint64_t>(d) + bytes - 1) >> 32);
     unsigned long long ref[9] = {0};
     const char* only = argc > 4 ? argv[4] : nullptr;
+    // round 2 (env): PERSIST_BYTES for LD 5/6 kernels; WINDOW_BYTES / HIT_RATIO: an L2
+    // access-policy window (persisting hits, streaming misses) over the region's first
+    // WINDOW_BYTES, with the persisting carve-out set to its maximum
+    const uint64_t persist_bytes = getenv("PERSIST_BYTES") ? strtoull(getenv("PERSIST_BYTES"), nullptr, 10) : 0;
+    cudaStream_t st = nullptr;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (getenv("WINDOW_BYTES")) {
+        int maxp = 0, maxw = 0;
+        CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0));
+        CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, 0));
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, maxp));
+        size_t setp = 0;
+        CK(cudaDeviceGetLimit(&setp, cudaLimitPersistingL2CacheSize));
+        cudaStreamAttrValue av = {};
+        size_t wb = strtoull(getenv("WINDOW_BYTES"), nullptr, 10);
+        if (wb > (size_t)maxw) wb = maxw;
+        av.accessPolicyWindow.base_ptr = d;
+        av.accessPolicyWindow.num_bytes = wb;
+        av.accessPolicyWindow.hitRatio = getenv("HIT_RATIO") ? atof(getenv("HIT_RATIO")) : 1.0f;
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+        fprintf(stderr, "{\"max_persisting_l2\": %d, \"persisting_limit_set\": %zu, \"max_window\": %d, "
+                "\"window_bytes\": %zu, \"hit_ratio\": %.3f}\n", maxp, setp, maxw, wb, av.accessPolicyWindow.hitRatio);
+    } else if (persist_bytes) {
+        int maxp = 0;
+        CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0));
+        if (!getenv("NO_PERSIST_LIMIT")) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, maxp));
+        fprintf(stderr, "{\"max_persisting_l2\": %d, \"persist_bytes\": %llu}\n", maxp,
+                (unsigned long long)persist_bytes);
+    }
     for (auto& v : variants) {
         if (only && strstr(v.name, only) == nullptr) continue;
         if (!v.straddle && straddles) continue;
@@ -135,15 +177,37 @@ int main(int argc, char** argv) {
         a.slice_shift = 0;
         while ((size_t(1) << a.slice_shift) < dyn) ++a.slice_shift;
         a.raw = raw;
+        a.persist_bytes = persist_bytes;
         sage::fill_tables(a, v.P);
+        const int grid = blocks * threads / (v.ilp * v.threads);
+        if (v.cluster) {
+            cudaLaunchConfig_t occ = {};
+            occ.gridDim = dim3(grid);
+            occ.blockDim = dim3(v.threads);
+            occ.dynamicSmemBytes = dyn;
+            cudaLaunchAttribute oat[1];
+            oat[0].id = cudaLaunchAttributeClusterDimension;
+            oat[0].val.clusterDim.x = v.cluster;
+            oat[0].val.clusterDim.y = 1;
+            oat[0].val.clusterDim.z = 1;
+            occ.attrs = oat;
+            occ.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, v.fn, &occ) == cudaSuccess)
+                fprintf(stderr, "{\"variant\": \"%s\", \"max_active_clusters\": %d, \"clusters_needed\": %d}\n",
+                        v.name, nclusters, grid / v.cluster);
+            else
+                cudaGetLastError();
+        }
         float best = 1e30f;
         unsigned long long h_raw[4];
         for (int rep = 0; rep < 3; ++rep) {
-            CK(cudaMemset(raw, 0, 32));
-            CK(cudaEventRecord(e0));
+            CK(cudaMemsetAsync(raw, 0, 32, st));
+            CK(cudaEventRecord(e0, st));
             if (v.cluster) {
                 cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = dim3(blocks);
+                cfg.stream = st;
+                cfg.gridDim = dim3(grid);
                 cfg.blockDim = dim3(threads);
                 cfg.dynamicSmemBytes = dyn;
                 cudaLaunchAttribute at[1];
@@ -155,9 +219,9 @@ int main(int argc, char** argv) {
                 cfg.numAttrs = 1;
                 CK(cudaLaunchKernelEx(&cfg, v.fn, a));
             } else {
-                v.fn<<<blocks * threads / (v.ilp * v.threads), v.threads, dyn>>>(a);
+                v.fn<<<grid, v.threads, dyn, st>>>(a);
             }
-            CK(cudaEventRecord(e1));
+            CK(cudaEventRecord(e1, st));
             CK(cudaEventSynchronize(e1));
             CK(cudaGetLastError());
             float ms;

@@ -102,21 +102,21 @@ uint32_t ilp_for(uint32_t P, bool smem, bool straddle, uint32_t blocks, uint32_t
 // rounds, 8 reserved registers (64 in all).
 constexpr int kHybridUnroll = 2, kHybridPad = 8;
 KernelFn hybrid_kernel() {
-    return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 8, 0, 0, false, 0, kIlpSmem, 0, kHybridPad>;
+    return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 8, false, kIlpSmem, kHybridPad>;
 }
 
 template <int P>
 KernelFn kernel_for_p(bool smem, bool straddle, uint32_t ilp) {
     if constexpr (P == 1) {
         if (ilp == kIlpSmem && smem && !straddle)
-            return sage::sage_checksum_kernel<1, true, false, XsSmem<1>::xs, kIlpUnroll, Addr<1>::mode, 0, 0, false, 0,
-                                              kIlpSmem, 0, kIlpPad>;
+            return sage::sage_checksum_kernel<1, true, false, XsSmem<1>::xs, kIlpUnroll, Addr<1>::mode, false, kIlpSmem,
+                                              kIlpPad>;
     }
     if (smem) {
-        return straddle ? sage::sage_checksum_kernel<P, true, true, 0, Unroll<P>::smem_straddle, 0, 0>
-                        : sage::sage_checksum_kernel<P, true, false, XsSmem<P>::xs, Unroll<P>::smem, Addr<P>::mode, 0>;
+        return straddle ? sage::sage_checksum_kernel<P, true, true, 0, Unroll<P>::smem_straddle, 0>
+                        : sage::sage_checksum_kernel<P, true, false, XsSmem<P>::xs, Unroll<P>::smem, Addr<P>::mode>;
     }
-    return sage::sage_checksum_kernel<P, false, true, kXsGlobal, Unroll<P>::global, 0, 0>;
+    return sage::sage_checksum_kernel<P, false, true, kXsGlobal, Unroll<P>::global, 0>;
 }
 
 KernelFn kernel_for(uint32_t P, bool smem, bool straddle, uint32_t ilp = 1) {
@@ -131,9 +131,9 @@ KernelFn kernel_for(uint32_t P, bool smem, bool straddle, uint32_t ilp = 1) {
 // Inclusion-experiment variant (counts reads per chunk); GLOBAL placement.
 KernelFn counting_kernel_for(uint32_t P) {
     switch (P) {
-        case 1: return sage::sage_checksum_kernel<1, false, true, 0, 1, 0, 0, 0, true>;
-        case 4: return sage::sage_checksum_kernel<4, false, true, 0, 1, 0, 0, 0, true>;
-        case 8: return sage::sage_checksum_kernel<8, false, true, 0, 1, 0, 0, 0, true>;
+        case 1: return sage::sage_checksum_kernel<1, false, true, 0, 1, 0, true>;
+        case 4: return sage::sage_checksum_kernel<4, false, true, 0, 1, 0, true>;
+        case 8: return sage::sage_checksum_kernel<8, false, true, 0, 1, 0, true>;
         default: return nullptr;
     }
 }

@@ -1,4 +1,4 @@
-// sage_kernel.cuh -- the SCS-2 checksum kernel for sm_100a.
+// sage_kernel.cuh -- the SCS-2 checksum kernel for sm_100a (product).
 //
 // One launch = one attestation (SAGE section 5.2.2).  Every logical
 // thread of a full-occupancy grid (2048 per SM: 2 CTAs x 1024 threads at 32
@@ -12,6 +12,9 @@
 //   SMEM   : the region is copied once per CTA into shared memory with a 1-D
 //            TMA bulk copy (cp.async.bulk + mbarrier complete_tx); each round's
 //            pick is one LDS.
+//   HYBRID : (ADDR 8) the first region_bytes of the region are staged as for
+//            SMEM, the rest is read in place; each pick loads from whichever
+//            holds it.
 //   GLOBAL : each round's pick is one read-only LDG (32/128/256-bit for
 //            P = 1/4/8) straight from L2/HBM; the data pointer of the pick is
 //            the load address itself.
@@ -21,13 +24,10 @@
 // IMAD (FMA pipe) and t = a + rotl(t, S) one LEA.HI-class op (ALU pipe),
 // the interleaved shift-and-add pattern of P:651.
 //
-// Template knobs of sage_checksum_kernel.  The product (sage_api.cu) uses
-// LD=0, EXTRA=0, COUNT=false (except sage_attest_coverage), ILP=1;
-// XS=16 for P=1 SMEM and for every GLOBAL kernel (XS=0 otherwise); and
-// ADDR=4 (P=1) / ADDR=2 (P=4) / ADDR=1 (P=8) for non-straddling SMEM regions;
-// the other values are lowering alternatives measured by bench/variants.cu and
-// bench/adversary.cu and kept so those measurements stay reproducible
-// (DESIGN.md section 8).
+// This header holds only the product's lowering choices (sage_api.cu picks
+// the instantiations).  The measurement knobs of round 1 (timing-adversary
+// injections, instruction-mix probes, alternative lowerings, traces) live in
+// the bench harness, bench/sage_lab.cuh.
 #pragma once
 #include <stdint.h>
 
@@ -104,46 +104,23 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 template <int P> struct Pick { uint32_t w[P]; };
 
-// Read-only global loads of one P-word chunk.  LD selects the cache policy:
-//   0: ld.global.nc                          (L1-allocating; small, L1-resident regions)
-//   1: ld.global.nc.L1::no_allocate          (no L1 allocation)
-//   2: ld.global.cg                          (cache at L2 only)
-//   3: ld.global.nc.L2::64B                  (64-B L2 fetch hint)
-//   4: ld.global.nc.L1::no_allocate.L2::cache_hint with an evict_first policy
-template <int P, int LD>
-__device__ __forceinline__ Pick<P> load_global(const uint32_t* p, uint64_t policy) {
+// Read-only global load of one P-word chunk (ld.global.nc: L1-allocating; small,
+// L1-resident regions are 6.8x faster than with L1 bypassed).
+template <int P>
+__device__ __forceinline__ Pick<P> load_global(const uint32_t* p) {
     Pick<P> d;
     uint32_t* w = d.w;
     if constexpr (P == 1) {
-        if constexpr (LD == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
-        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
-        else if constexpr (LD == 2) asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
-        else if constexpr (LD == 3) asm volatile("ld.global.nc.L2::64B.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
-        else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(w[0]) : "l"(p), "l"(policy));
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
     } else if constexpr (P == 4) {
-#define O4 "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-        if constexpr (LD == 0) asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
-        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
-        else if constexpr (LD == 2) asm volatile("ld.global.cg.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
-        else if constexpr (LD == 3) asm volatile("ld.global.nc.L2::64B.v4.b32 {%0,%1,%2,%3}, [%4];" : O4 : "l"(p));
-        else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;" : O4 : "l"(p), "l"(policy));
-#undef O4
+        asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "l"(p));
     } else {
-#define O8 "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-        if constexpr (LD == 0) asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
-        else if constexpr (LD == 1) asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
-        else if constexpr (LD == 2) asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
-        else if constexpr (LD == 3) asm volatile("ld.global.nc.L2::64B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : O8 : "l"(p));
-        else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;" : O8 : "l"(p), "l"(policy));
-#undef O8
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                     : "l"(p));
     }
     return d;
-}
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
 }
 
 template <int P>
@@ -181,95 +158,51 @@ struct KernelArgs {
     uint64_t nonce;
     uint32_t nc_mask;         // Nc - 1
     uint32_t rounds;          // R
-    uint32_t region_bytes;    // SMEM staging size (SMEM placement only)
+    uint32_t region_bytes;    // bytes staged in shared memory (SMEM / HYBRID placement)
     uint64_t* raw;            // [checksum, max cycles, ~min start ns, max end ns]
     uint64_t* per_warp;       // optional, n/32 partial sums
     // R7 multipliers MUL[j] = 2^L[j] + 1, passed through the constant bank so
     // ptxas emits one IMAD R, R, c[..], R per step instead of strength-reducing
     // a*(2^L+1)+t into a*2^L + (a+t) (two FMA-pipe ops).
     uint32_t mul[kAccum];
-    // 2^20, 2^25, 2^5: xorshift shift multipliers for the IMAD.WIDE lowering
-    // (constant bank, so ptxas cannot turn them back into ALU shifts).
-    uint32_t p2[3];
     uint32_t four_p;          // 4*P as a runtime value (forces IMAD for the chunk offset)
-    uint32_t zero;            // 0; operand of the injected instructions of EXTRA > 0 (timing adversary)
-    uint32_t one;             // 1; multiplier that keeps an add on the FMA pipe (ADDR = 2)
+    uint32_t zero;            // 0; operand of the register reservation's result-neutral fold (PAD)
+    uint32_t one;             // 1; multiplier that keeps an add on the FMA pipe (ADDR 2/4/8)
     uint32_t* counts;         // COUNT variant only: per-chunk read counters (inclusion experiment)
-    uint64_t* cta_trace;      // optional: per CTA {smid, start ns, end ns, clock64 span} (diagnostics)
-    uint32_t slice_shift;     // ADDR == 3 (cluster-distributed SMEM): log2 of the bytes each CTA holds
-    uint64_t* progress;       // PROBE bit 5 only: per CTA, %globaltimer every progress_every trips
-    uint32_t progress_every;  //   (progress[blockIdx.x * progress_slots + k]); diagnostics
-    uint32_t progress_slots;
 };
 
 // The region staged in shared memory (SMEM placement): namespace-scope so the
 // round can address it with a constant base (LDS [v + const]).
 extern __shared__ __align__(128) uint32_t smem_words[];
 
-// R1 state step with a selectable lowering of each 64-bit shift-xor.
-// XS bit k set => step k uses IMAD.WIDE.U32 by 2^s on the FMA pipe to
-// produce both 32-bit halves of the cross-word shift, instead of the funnel
-// shift on the ALU pipe.  Same function either way (xorshift64 (12,25,27)).
-template <int XS>
-__device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const KernelArgs& args) {
-    // x ^= x >> 12
-    if constexpr (XS & 8) {
-        lo = lo ^ __funnelshift_r(lo, hi, 12);
-        hi = hi ^ __umulhi(hi, args.p2[0]);                                // hi >> 12 on the FMA pipe
-    } else if constexpr (XS & 1) {
-        const uint64_t w = static_cast<uint64_t>(hi) * args.p2[0];         // {hi << 20, hi >> 12}
-        lo = lo ^ (lo >> 12) ^ static_cast<uint32_t>(w);
-        hi = hi ^ static_cast<uint32_t>(w >> 32);
-    } else {
-        lo = lo ^ __funnelshift_r(lo, hi, 12);
-        hi = hi ^ (hi >> 12);
-    }
-    // x ^= x << 25
-    if constexpr (XS & 2) {
-        const uint64_t w = static_cast<uint64_t>(lo) * args.p2[1];         // {lo << 25, lo >> 7}
-        hi = hi ^ (hi << 25) ^ static_cast<uint32_t>(w >> 32);
-        lo = lo ^ static_cast<uint32_t>(w);
-    } else {
-        hi = hi ^ __funnelshift_l(lo, hi, 25);
-        lo = lo ^ (lo << 25);
-    }
-    // x ^= x >> 27
-    if constexpr (XS & 8) {
-        lo = lo ^ __funnelshift_r(lo, hi, 27);
-        hi = hi ^ __umulhi(hi, args.p2[2]);                                // hi >> 27 on the FMA pipe
-    } else if constexpr (XS & 4) {
-        const uint64_t w = static_cast<uint64_t>(hi) * args.p2[2];         // {hi << 5, hi >> 27}
-        lo = lo ^ (lo >> 27) ^ static_cast<uint32_t>(w);
-        hi = hi ^ static_cast<uint32_t>(w >> 32);
-    } else {
-        lo = lo ^ __funnelshift_r(lo, hi, 27);
-        hi = hi ^ (hi >> 27);
-    }
-}
-
-// One SCS-2 round (R1-R9) for this thread.
-//   P        words per pick (1, 4, 8)
-//   SMEM     region in shared memory (else read from global)
-//   STRADDLE the region's chunk addresses may differ in their high 32 bits
-//            (else hi32(dp) == hi32(base) for every chunk, host-checked)
-//   XS       xorshift lowering (see xorshift_split)
-//   EXTRA    number of result-neutral instructions injected (when `inject`) into
-//            the round (0 in the product; > 0 only for the timing-adversary
-//            experiment, the B200 analogue of Table 1 Exp 2's
-//            "adversarial NOP"; the kernel injects them every EVERY
-//            rounds of the unrolled trip, or in its first round when EVERY = 0)
-//   COUNT    also count reads per chunk into args.counts (the memory-region
-//            inclusion experiment, P:747-749; SURVEY 8(f) #2); not in the timed path
 // SCS-2 R6 / R9 odd multipliers: round index, high DP word, exchanged value.
 constexpr uint32_t kKR = 0x9E3779B1u, kKH = 0x85EBCA77u, kKX = 0xC2B2AE3Du;
 
-template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false,
-          int PROBE = 0>
+// One SCS-2 round (R1-R9) for this thread.
+//   P        words per pick (1, 4, 8)
+//   SMEM     region (or, ADDR 8, its staged prefix) in shared memory, else read from global
+//   STRADDLE the region's chunk addresses may differ in their high 32 bits
+//            (else hi32(dp) == hi32(base) for every chunk, host-checked)
+//   XS       16: y = x * M64 as one wide multiply and two chained IMADs; 0: as ptxas lowers it
+//   ADDR     pick addressing of non-straddling SMEM regions:
+//            0 generic, 1 chunk offset as IMAD, 2 offsets and the R6 add as IMADs,
+//            4 the warp-uniform R6 bracket folded into the chunk-offset IMAD,
+//            8 SAGE_HYBRID (staged prefix in shared memory, the rest from global)
+//   COUNT    also count reads per chunk into args.counts (the memory-region
+//            inclusion experiment, P:747-749; SURVEY 8(f) #2); not in the timed path
+template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR, bool COUNT>
 __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
-                                           const KernelArgs& args, uint64_t policy = 0, bool inject = false) {
+                                           const KernelArgs& args) {
+    static_assert(XS == 0 || XS == 16, "product xorshift lowerings");
+    static_assert(ADDR == 0 || ADDR == 1 || ADDR == 2 || ADDR == 4 || ADDR == 8, "product pick addressings");
     // R1
-    xorshift_split<XS>(xlo, xhi, args);
+    xlo = xlo ^ __funnelshift_r(xlo, xhi, 12);              // x ^= x >> 12
+    xhi = xhi ^ (xhi >> 12);
+    xhi = xhi ^ __funnelshift_l(xlo, xhi, 25);              // x ^= x << 25
+    xlo = xlo ^ (xlo << 25);
+    xlo = xlo ^ __funnelshift_r(xlo, xhi, 27);              // x ^= x >> 27
+    xhi = xhi ^ (xhi >> 27);
     uint64_t y;
     if constexpr (XS & 16) {
         // y = x * M64 (mod 2^64) as one wide multiply and two chained multiply-adds
@@ -293,67 +226,17 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
     // R4, R5, R6 (first part)
     Pick<P> d;
     uint32_t t;
-    if constexpr (SMEM && !STRADDLE && ADDR == 3) {
-        // region distributed over the cluster's shared memories: CTA rank k holds
-        // bytes [k << slice_shift, (k+1) << slice_shift); read through DSMEM
-        const uint32_t v = i * args.four_p;
-        const uint32_t owner = v >> args.slice_shift;
-        const uint32_t local = smem_u32(smem_words) + (v & ((1u << args.slice_shift) - 1u));
-        uint32_t raddr;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(local), "r"(owner));
-        if constexpr (P == 1) {
-            asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(d.w[0]) : "r"(raddr) : "memory");
-        } else {
-#pragma unroll
-            for (int h = 0; h < P / 4; ++h)
-                asm volatile("ld.shared::cluster.v4.b32 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(d.w[4 * h]), "=r"(d.w[4 * h + 1]), "=r"(d.w[4 * h + 2]), "=r"(d.w[4 * h + 3])
-                             : "r"(raddr + 16 * h) : "memory");
-        }
-        t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
-    } else if constexpr (SMEM && !STRADDLE && ADDR == 4) {
+    if constexpr (SMEM && !STRADDLE && ADDR == 4) {
         // as ADDR == 2, with the whole warp-uniform bracket folded into the chunk-offset IMAD
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
-        if constexpr (PROBE & 1) d.w[0] = addr;                 // probe only: no shared-memory load
-        else d = load_shared_addr<P>(addr);
+        d = load_shared_addr<P>(addr);
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
-    } else if constexpr (SMEM && !STRADDLE && ADDR == 7) {
-        // hybrid placement: the first region_bytes of the region are staged in shared
-        // memory, the rest is read from global (L1/L2); each lane loads from whichever
-        // holds its chunk (predicated LDS / LDG, so a lane touches one of the two)
-        const uint32_t v = i * args.four_p;
-        const uint32_t saddr = v + smem_u32(smem_words);
-        const uint64_t gaddr = base + v;
-        const uint32_t staged = args.region_bytes;
-        if constexpr (P == 1) {
-            asm volatile("{\n\t.reg .pred p;\n\t"
-                         "setp.lt.u32 p, %1, %2;\n\t"
-                         "@p ld.shared.b32 %0, [%3];\n\t"
-                         "@!p ld.global.nc.b32 %0, [%4];\n\t}"
-                         : "=r"(d.w[0]) : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
-        } else if constexpr (P == 4) {
-            asm volatile("{\n\t.reg .pred p;\n\t"
-                         "setp.lt.u32 p, %4, %5;\n\t"
-                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%6];\n\t"
-                         "@!p ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%7];\n\t}"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3])
-                         : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
-        } else {
-            asm volatile("{\n\t.reg .pred p;\n\t"
-                         "setp.lt.u32 p, %8, %9;\n\t"
-                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%10];\n\t"
-                         "@p ld.shared.v4.b32 {%4,%5,%6,%7}, [%10+16];\n\t"
-                         "@!p ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%11];\n\t}"
-                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
-                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7])
-                         : "r"(v), "r"(staged), "r"(saddr), "l"(gaddr));
-        }
-        t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
     } else if constexpr (SMEM && !STRADDLE && ADDR == 8) {
-        // hybrid placement as ADDR == 7 with the address arithmetic on the FMA pipe:
-        // shared address and 64-bit global address as IMAD / IMAD.WIDE, and the R6
-        // bracket folded as in ADDR == 4
+        // hybrid placement: chunks below region_bytes are staged in shared memory, the
+        // rest is read from global (L1/L2); each lane issues a predicated LDS or LDG for
+        // its own pick.  Shared address and 64-bit global address as IMAD / IMAD.WIDE
+        // (FMA pipe), the R6 bracket folded as in ADDR == 4.
         const uint32_t saddr = i * args.four_p + smem_u32(smem_words);
         const uint64_t gaddr = static_cast<uint64_t>(i) * args.four_p + base;
         const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
@@ -365,19 +248,6 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                      "@!p ld.global.nc.b32 %0, [%4];\n\t}"
                      : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
-    } else if constexpr (SMEM && !STRADDLE && ADDR == 5) {
-        // lo32(y) + 4P*i in one IMAD, then the warp-uniform bracket
-        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
-        const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
-        d = load_shared_addr<P>(addr);
-        t = (i * args.four_p + static_cast<uint32_t>(y)) + ur;
-    } else if constexpr (SMEM && !STRADDLE && ADDR == 6) {
-        // lo32(y)*1 + addr (FMA pipe), then the warp-uniform bracket (which absorbs -smem)
-        const uint32_t addr = i * args.four_p + smem_u32(smem_words);
-        const uint32_t ur = r * kKR + (static_cast<uint32_t>(base) - smem_u32(smem_words)) +
-                            static_cast<uint32_t>(base >> 32) * kKH;
-        d = load_shared_addr<P>(addr);
-        t = (static_cast<uint32_t>(y) * args.one + addr) + ur;
     } else if constexpr (SMEM && !STRADDLE && ADDR == 2) {
         // both chunk offsets and the R6 add as IMADs (FMA pipe), sparing the ALU pipe
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
@@ -399,7 +269,7 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
     } else {
         const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);   // R5 (= the global load address)
         if constexpr (SMEM) d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
-        else d = load_global<P, LD>(reinterpret_cast<const uint32_t*>(dp), policy);
+        else d = load_global<P>(reinterpret_cast<const uint32_t*>(dp));
         t = static_cast<uint32_t>(y) + r * kKR + static_cast<uint32_t>(dp) + static_cast<uint32_t>(dp >> 32) * kKH;
     }
     // R6 (data)
@@ -411,48 +281,26 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         a[j] = a[j] * args.mul[j] + t;
         t = a[j] + rotl(t, rot_of(j));
     }
-    // injected adversary work: dependent ALU ops that leave t unchanged (t ^ 0)
-    if (inject) {
-        // EXTRA > 0: dependent ALU-pipe ops (t ^ 0); EXTRA < 0: dependent FMA-pipe ops (t * 1)
-#pragma unroll
-        for (int e = 0; e < (EXTRA > 0 ? EXTRA : -EXTRA); ++e) {
-            if constexpr (EXTRA > 0) t ^= args.zero;
-            else t = t * args.one;
-        }
-    }
     // R8
     t = t + (t >> (C & 31u));
     // R9 (SCS-2: multiply-add exchange)
-    if constexpr (PROBE & 2) a[kAccum - 1] = a[kAccum - 1] * kKX + t;    // probe only: no exchange
-    else a[kAccum - 1] = a[kAccum - 1] * kKX + __shfl_sync(0xFFFFFFFFu, t, src_lane);
+    a[kAccum - 1] = a[kAccum - 1] * kKX + __shfl_sync(0xFFFFFFFFu, t, src_lane);
 }
 
-//   PROBE    measurement-only instruction-mix probes (never in the product; the
-//            checksum is then not SCS-2): bit 0 replaces the pick's shared-memory
-//            load by its address (ADDR == 4 only), bit 1 the neighbour exchange by
-//            the lane's own t, so the loop keeps only its integer arithmetic;
-//            bit 2 (result-neutral, ILP > 1) staggers the lane states: each state's
-//            round starts with x += a'[0] * 0 (bit 3: a'[8]) on the other state's
-//            accumulator, an FMA-pipe dependency that offsets the two chains;
-//            bit 4 (result-neutral) emits the unrolled trip lane-state-major;
-//            bit 5 (result-neutral) stamps a per-CTA progress trace (args.progress)
-//   PAD      registers reserved (kept live across the round loop, unused) so that
-//            an ILP > 1 kernel allocates the whole register file (see DESIGN.md 8)
-//   SYNC     > 0: a CTA barrier every SYNC trips of the round loop (result-neutral;
-//            bounds how far the warps of a CTA drift apart before the final reduction)
-//   FEXTRA   timing adversary only (0 in the product): the adversary's own work
-//            alongside the checksum, |FEXTRA| dependent ops per round per lane
-//            state on a chain independent of the checksum state -- FFMA (FP32,
-//            either FMA pipe) for FEXTRA > 0, IMAD (FMA-heavy pipe) for FEXTRA < 0;
-//            folded into the result as (value & 0), so the checksum is unchanged
+// The checksum kernel (one attestation per launch).
+//   UNROLL   rounds per trip of the round loop (remainder rounds run one by one)
 //   ILP      logical SCS-2 warps per hardware warp: 1 = one lane state per
 //            thread, 2 CTAs x 1024 threads per SM at 32 registers; 2 = two
 //            independent lane states per thread (interleaved by ptxas), one
 //            CTA x 1024 threads per SM at 57-64 registers (64 allocated) -- the same register file
 //            and logical grid, but all 32 warps of the SM progress together.
-template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
-          bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0, int SYNC = 0, int FEXTRA = 0>
-__global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
+//   PAD      registers reserved (kept live across the round loop, unused) so that
+//            an ILP > 1 kernel allocates the whole register file (see DESIGN.md 8)
+// UNROLL and PAD do not change the arithmetic; they steer ptxas' schedule
+// (schedule search).
+template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR, bool COUNT = false, int ILP = 1, int PAD = 0>
+__global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
+    static_assert(ILP == 1 || ILP == 2, "one or two lane states per thread");
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint64_t t_start_ns;
@@ -464,7 +312,7 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
         c_start = clock64();
     }
 
-    // a2: stage the region into shared memory (SMEM placement).
+    // a2: stage the region (or its prefix, HYBRID) into shared memory.
     if constexpr (SMEM) {
         const uint32_t bytes = args.region_bytes;
         if ((bytes & 15u) == 0) {
@@ -472,23 +320,14 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
             __syncthreads();
             if (threadIdx.x == 0) {
                 mbar_expect_tx(&bar, bytes);
-                uint32_t src0 = 0;                       // ADDR == 3: this CTA's slice of the region
-                if constexpr (ADDR == 3) {
-                    uint32_t rank;
-                    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-                    src0 = rank * bytes;
-                }
                 constexpr uint32_t kChunk = 32768;
                 for (uint32_t off = 0; off < bytes; off += kChunk) {
                     const uint32_t n = (bytes - off < kChunk) ? (bytes - off) : kChunk;
-                    bulk_g2s(reinterpret_cast<char*>(smem_words) + off,
-                             reinterpret_cast<const char*>(args.region) + src0 + off, n, &bar);
+                    bulk_g2s(reinterpret_cast<char*>(smem_words) + off, reinterpret_cast<const char*>(args.region) + off,
+                             n, &bar);
                 }
             }
             mbar_wait(&bar, 0);
-            if constexpr (ADDR == 3) {                   // every slice staged before any remote read
-                asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-            }
         } else {  // 4- or 8-byte regions: below the bulk-copy granule
             for (uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x) smem_words[k] = args.region[k];
             __syncthreads();
@@ -531,74 +370,24 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
     const uint64_t base = reinterpret_cast<uint64_t>(args.region);
     const uint32_t nc_mask = args.nc_mask;
     const uint32_t rounds = args.rounds;
-    uint64_t policy = 0;
-    if constexpr (LD == 4) policy = evict_first_policy();
 
-    // a10: round loop, UNROLL rounds per trip + remainder
+    // a10: round loop, UNROLL rounds (of every lane state) per trip + remainder
     uint32_t r = 0;
     const uint32_t main_end = rounds - rounds % UNROLL;
-    uint32_t trips_to_sync = SYNC;
-    float fadv[ILP];                                   // FEXTRA > 0: the adversary's FP32 chain
-    uint32_t iadv[ILP];                                // FEXTRA < 0: the adversary's integer chain
-#pragma unroll
-    for (int s = 0; s < ILP; ++s) {
-        fadv[s] = static_cast<float>(lane + s);
-        iadv[s] = lane + s;
-    }
-    [[maybe_unused]] uint32_t trip = 0;
     for (; r < main_end; r += UNROLL) {
-        if constexpr (PROBE & 32) {
-            // progress trace (diagnostics, result-neutral): thread 0 stamps %globaltimer
-            if (threadIdx.x == 0 && trip % args.progress_every == 0) {
-                const uint32_t k = trip / args.progress_every;
-                if (k < args.progress_slots) args.progress[static_cast<uint64_t>(blockIdx.x) * args.progress_slots + k] =
-                    globaltimer();
-            }
-            ++trip;
-        }
-        if constexpr (SYNC > 0) {
-            // keep the CTA's warps within SYNC trips of each other (result-neutral)
-            if (--trips_to_sync == 0) {
-                trips_to_sync = SYNC;
-                __syncthreads();
-            }
-        }
 #pragma unroll
         for (int uu = 0; uu < UNROLL * ILP; ++uu) {
-            // source order of the unrolled trip: round-major (u, s) by default;
-            // PROBE bit 4 (result-neutral) emits it lane-state-major (s, u) instead
-            const int u = (PROBE & 16) ? uu % UNROLL : uu / ILP;
-            const int s = (PROBE & 16) ? uu / UNROLL : uu % ILP;
-            {
-                if constexpr (ILP > 1 && (PROBE & 4)) {
-                    // stagger: a result-neutral FMA-pipe dependency (x += a'[K] * 0) on a
-                    // value the other lane state produces early in its last round
-                    constexpr int kDep = (PROBE & 8) ? 8 : 0;
-                    xlo[s] = a[(s + ILP - 1) % ILP][kDep] * args.zero + xlo[s];
-                }
-                scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(
-                    a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
-                    EVERY > 0 ? (u % EVERY == 0) : (u == 0));
-#pragma unroll
-                for (int e = 0; e < (FEXTRA > 0 ? FEXTRA : -FEXTRA); ++e) {
-                    if constexpr (FEXTRA > 0) fadv[s] = fmaf(fadv[s], 1.0001f, 0.5f);
-                    else iadv[s] = iadv[s] * args.mul[e & 15] + args.one;
-                }
-            }
+            const int u = uu / ILP;                     // round-major: (u, s)
+            const int s = uu % ILP;
+            scs_round<P, SMEM, STRADDLE, XS, ADDR, COUNT>(a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args);
         }
     }
     for (; r < rounds; ++r) {
 #pragma unroll
         for (int s = 0; s < ILP; ++s)
-            scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
-                                                                      args, policy, true);
+            scs_round<P, SMEM, STRADDLE, XS, ADDR, COUNT>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane, args);
     }
 
-    if constexpr (FEXTRA != 0) {
-#pragma unroll
-        for (int s = 0; s < ILP; ++s)          // keep the adversary's chain live: xlo ^= v & 0
-            xlo[s] ^= (FEXTRA > 0 ? __float_as_uint(fadv[s]) : iadv[s]) & args.zero;
-    }
     if constexpr (PAD > 0) {
 #pragma unroll
         for (int k = 0; k < PAD; ++k)          // xlo ^= pad & 0 (args.zero): result-neutral
@@ -637,19 +426,7 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
                       static_cast<unsigned long long>(~t_start_ns));
             atomicMax(reinterpret_cast<unsigned long long*>(&args.raw[3]),
                       static_cast<unsigned long long>(t_end_ns));
-            if (args.cta_trace) {
-                uint32_t smid;
-                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                uint64_t* tr = args.cta_trace + 4ull * blockIdx.x;
-                tr[0] = smid;
-                tr[1] = t_start_ns;
-                tr[2] = t_end_ns;
-                tr[3] = static_cast<uint64_t>(c_end - c_start);
-            }
         }
-    }
-    if constexpr (ADDR == 3) {                           // keep this CTA's slice alive for remote readers
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 }
 
@@ -659,9 +436,6 @@ inline void fill_tables(KernelArgs& args, uint32_t P) {
     args.zero = 0;
     args.one = 1;
     for (int j = 0; j < kAccum; ++j) args.mul[j] = mul_of(j);
-    args.p2[0] = 1u << 20;
-    args.p2[1] = 1u << 25;
-    args.p2[2] = 1u << 5;
 }
 
 }  // namespace sage
