@@ -77,15 +77,26 @@ def H(x):
     return hashlib.sha256(x).digest()
 
 
-def mac(key_material, msg):
-    """AES-CMAC with key SHA-256(key_material)[0:16]."""
-    c = cmac.CMAC(algorithms.AES(hashlib.sha256(key_material).digest()[:16]))
+def mac_key(key_material):
+    """The 128-bit AES-CMAC key derived from key material: SHA-256(key_material)[0:16]."""
+    return hashlib.sha256(key_material).digest()[:16]
+
+
+def cmac_aes128(key16, msg):
+    """AES-CMAC (RFC 4493) under a 16-byte key."""
+    c = cmac.CMAC(algorithms.AES(bytes(key16)))
     c.update(msg)
     return c.finalize()
 
 
+def mac(key_material, msg):
+    """MAC of SAKE: AES-CMAC under mac_key(key_material)."""
+    return cmac_aes128(mac_key(key_material), msg)
+
+
 def mac_ok(key_material, msg, tag):
-    c = cmac.CMAC(algorithms.AES(hashlib.sha256(key_material).digest()[:16]))
+    """Constant-time check of a tag produced by mac()."""
+    c = cmac.CMAC(algorithms.AES(mac_key(key_material)))
     c.update(msg)
     try:
         c.verify(tag)

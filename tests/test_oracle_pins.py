@@ -2,8 +2,8 @@
 
 Each test states what it pins and where the fact comes from.  Expected values
 are published constants, hand-derived values for degenerate inputs, algebraic
-invariants of SCS-1, or brute force on tiny inputs --
-never the oracle's own output.  P:n = PAPER.md line n, S:n = SPEC.md line n.
+invariants of SCS-2, statistics the paper's design fixes,
+or brute force on tiny inputs -- never the oracle's own output.  P:n = PAPER.md line n, S:n = SPEC.md line n.
 """
 import numpy as np
 import pytest
@@ -223,7 +223,8 @@ def test_self_modify_shift_examples():
 
 
 def test_neighbour_exchange_direction():
-    """R9 (north_star, Q13): lane l XORs lane (l+1) mod 32's t into a[15] only.
+    """R9 (north_star, Q13): lane l folds lane (l+1) mod 32's t into a[15] only
+    (SCS-2: a[15] <- a[15]*KX + t_{l+1}).
     Perturbing lane k changes lane k's state and only a[15] of lane k-1."""
     rng = np.random.default_rng(3)
     region = rng.integers(0, 256, 1024, dtype=np.uint8)
@@ -382,3 +383,177 @@ def test_data_pointer_scales_with_pick_words():
             for _ in range(P):
                 t = (rotl(t, 5) + i) & M32
             assert int(A2[0, 0]) == t, (P, C)
+
+
+# ------------------------------------------- R4-R7 injectivity, exhaustive at R = 1
+def _picks_by_formula(A, X, nc):
+    """R1-R3 written out independently: lane l's chunk index for one round."""
+    out = []
+    for lane in range(32):
+        x = int(X[lane])
+        x ^= x >> 12
+        x ^= (x << 25) & M64
+        x ^= x >> 27
+        y = (x * XS_MULT_DEC) & M64
+        out.append(((y >> 32) ^ int(A[lane, 15])) & (nc - 1))
+    return out
+
+
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_single_round_injectivity_exhaustive(P):
+    """SURVEY 8(c) R6-R7 pin, exhaustive over a 64-word region at R = 1: for a fixed
+    pre-round state and pick, t after R6 is a bijection of each loaded word (rotl
+    then add), and a[0] <- a[0]*MUL[0] + t a bijection of t.  So for EVERY one of
+    the 64 x 32 single-bit flips of the region, a[0] changes in exactly the lanes
+    whose pick contained the flipped word -- deterministically, after one round --
+    and in no other lane; every other lane keeps its whole state except a[15] of
+    the lane to the left of a picking lane (R9 takes its neighbour's t).  The
+    picking lanes come from R1-R3 retyped here, and every lane must pick exactly
+    one chunk (the flips reaching it all lie in one P-word chunk)."""
+    rng = np.random.default_rng(100 + P)
+    nwords = 64
+    nc = nwords // P
+    region = rng.integers(0, 256, 4 * nwords, dtype=np.uint8)
+    base = 0x7F3A_0000_2000
+    A0 = rng.integers(0, 2**32, (32, 16), dtype=np.uint64).astype(np.uint32)
+    X0 = rng.integers(1, 2**64 - 1, 32, dtype=np.uint64)
+    r = 77
+    ref, refx = oracle.warp_rounds(A0, X0, region, base, r, r + 1, P=P)
+    picks = _picks_by_formula(A0, X0, nc)
+    reached = {lane: set() for lane in range(32)}
+    for bit in range(32 * nwords):
+        k = bit // 32
+        reg = region.copy()
+        reg[4 * k + (bit % 32) // 8] ^= 1 << (bit % 8)
+        out, outx = oracle.warp_rounds(A0, X0, reg, base, r, r + 1, P=P)
+        assert np.array_equal(outx, refx)
+        pickers = {lane for lane in range(32) if picks[lane] == k // P}
+        changed = {lane for lane in range(32) if out[lane, 0] != ref[lane, 0]}
+        assert changed == pickers, (bit, sorted(changed), sorted(pickers))
+        left = {(lane - 1) % 32 for lane in pickers}
+        for lane in range(32):
+            if lane in pickers:
+                reached[lane].add(k // P)
+            elif lane in left:
+                assert np.array_equal(out[lane, :15], ref[lane, :15]) and out[lane, 15] != ref[lane, 15]
+            else:
+                assert np.array_equal(out[lane], ref[lane])
+    assert all(len(v) == 1 for v in reached.values())
+
+
+# --------------------------------------------------- R8 shift amount uniformity
+def test_self_modify_shift_amount_is_uniform():
+    """S:228-230 (R8): N = C mod 32 with C the round-start a[15] is uniform over
+    0..31: chi-square over 10^5 (lane, round) samples of a seeded warp, 31 degrees of
+    freedom, below the 0.1% critical value 61.1; every value of N occurs."""
+    rng = np.random.default_rng(8)
+    region = rng.integers(0, 256, 4096, dtype=np.uint8)
+    A, X = [], []
+    for lane in range(32):
+        a, x = oracle.thread_init(0x5EED, lane)
+        A.append(a)
+        X.append(x)
+    A = np.array(A, dtype=np.uint32)
+    X = np.array(X, dtype=np.uint64)
+    counts = np.zeros(32, dtype=np.int64)
+    rounds = 100_000 // 32 + 1
+    for r in range(rounds):
+        counts += np.bincount(A[:, 15] & 31, minlength=32)
+        A, X = oracle.warp_rounds(A, X, region, 0x10000, r, r + 1, P=1)
+    n = counts.sum()
+    assert n >= 100_000
+    chi2 = float((((counts - n / 32) ** 2) / (n / 32)).sum())
+    assert chi2 < 61.1 and counts.min() > 0, (chi2, counts)
+
+
+# ------------------------------- SCS-2's odd multipliers KR, KH, KX are permutations
+class _FastRound:
+    """One-round oracle calls with preallocated ctypes buffers (2^20 of them per test)."""
+
+    def __init__(self, region):
+        import ctypes
+        self.ct = ctypes
+        self.L = oracle.lib()
+        self.region = np.ascontiguousarray(region, dtype=np.uint8)
+        self.A = np.zeros((32, 16), dtype=np.uint32)
+        self.X = np.zeros(32, dtype=np.uint64)
+        self.pa = self.A.ctypes.data_as(ctypes.c_void_p)
+        self.px = self.X.ctypes.data_as(ctypes.c_void_p)
+        self.pr = self.region.ctypes.data_as(ctypes.c_void_p)
+
+    def __call__(self, A0, X0, base, r):
+        self.A[:] = A0
+        self.X[:] = X0
+        rc = self.L.sage_oracle_warp_rounds(self.pa, self.px, self.pr, self.region.nbytes, base, r, r + 1, 1)
+        assert rc == 0
+        return self.A
+
+
+def _rotr(v, s):
+    return ((v >> s) | (v << (32 - s))) & M32
+
+
+def test_odd_multipliers_are_permutations_of_z_2_32():
+    """KR, KH, KX (and MUL[15] = 2^21 + 1) are odd, hence units of Z/2^32: v -> v*K mod 2^32
+    is a permutation.  Exhaustive on 2^20 inputs: the images are distinct, and the
+    modular inverse K^-1 (K * K^-1 = 1 mod 2^32) maps every image back to its input."""
+    v = np.arange(1 << 20, dtype=np.uint64)
+    for K in (KR, KH, KX, (1 << L_TAB[15]) + 1):
+        assert K % 2 == 1
+        Kinv = pow(K, -1, 1 << 32)
+        assert (K * Kinv) & M32 == 1
+        img = (v * np.uint64(K)) & np.uint64(M32)
+        assert np.unique(img).size == v.size
+        assert np.array_equal((img * np.uint64(Kinv)) & np.uint64(M32), v)
+
+
+def test_round_index_enters_as_a_permutation():
+    """R6 (Q10): the round index enters t as r*KR.  On a degenerate warp
+    (a = 0, one-chunk region, so a[0]' = rotl(t, 5) + w) the difference
+    rotr(a[0]'(r) - w, 5) - rotr(a[0]'(0) - w, 5) decoded with KR^-1 returns r for
+    every r < 2^20: the oracle's r -> a[0]' map is injective, exactly r*KR + const."""
+    w = 0x6A09E667
+    region = np.frombuffer(w.to_bytes(4, "little"), dtype=np.uint8)
+    run = _FastRound(region)
+    A0, X0 = _zero_state()
+    Kinv = pow(KR, -1, 1 << 32)
+    t0 = _rotr((int(run(A0, X0, 0, 0)[0, 0]) - w) & M32, 5)
+    for r in range(1, 1 << 20):
+        t = _rotr((int(run(A0, X0, 0, r)[0, 0]) - w) & M32, 5)
+        assert ((t - t0) * Kinv) & M32 == r, r
+
+
+def test_data_pointer_high_word_enters_as_a_permutation():
+    """R5-R6 (Q9): hi32(dp) enters t as hi32(dp)*KH.  With base = h << 32
+    (one chunk, so dp = base) the difference against h = 0 decoded with KH^-1 returns h
+    for every h < 2^20."""
+    w = 0xBB67AE85
+    region = np.frombuffer(w.to_bytes(4, "little"), dtype=np.uint8)
+    run = _FastRound(region)
+    A0, X0 = _zero_state()
+    Kinv = pow(KH, -1, 1 << 32)
+    t0 = _rotr((int(run(A0, X0, 0, 5)[0, 0]) - w) & M32, 5)
+    for h in range(1, 1 << 20):
+        t = _rotr((int(run(A0, X0, h << 32, 5)[0, 0]) - w) & M32, 5)
+        assert ((t - t0) * Kinv) & M32 == h, h
+
+
+def test_exchange_multiplier_is_a_permutation():
+    """R7[15] + R9 (Q13): lane 0's a[15]' = (a[15]*MUL[15] + t_15)*KX + t_{lane 1}, and
+    lane 1 does not depend on lane 0, so changing lane 0's a[15] by v changes its
+    a[15]' by v*MUL[15]*KX.  With a one-chunk region (the pick cannot move) the
+    difference decoded with (MUL[15]*KX)^-1 returns v for every v < 2^20 (all 32-bit
+    residues of the form covered: the map is a permutation)."""
+    rng = np.random.default_rng(15)
+    region = rng.integers(0, 256, 4, dtype=np.uint8)
+    run = _FastRound(region)
+    A0 = rng.integers(0, 2**32, (32, 16), dtype=np.uint64).astype(np.uint32)
+    X0 = rng.integers(1, 2**63, 32, dtype=np.uint64)
+    A0[0, 15] = 0
+    Kinv = pow(((1 << L_TAB[15]) + 1) * KX, -1, 1 << 32)
+    ref = int(run(A0, X0, 0x4000, 9)[0, 15])
+    A = A0.copy()
+    for v in range(1, 1 << 20):
+        A[0, 15] = v
+        out = int(run(A, X0, 0x4000, 9)[0, 15])
+        assert ((out - ref) * Kinv) & M32 == v, v

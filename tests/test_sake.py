@@ -7,8 +7,6 @@ import random
 import mpmath
 import numpy as np
 import pytest
-from cryptography.hazmat.primitives import cmac
-from cryptography.hazmat.primitives.ciphers import algorithms
 
 import oracle
 from paper_2209_03125_b200 import sake
@@ -45,11 +43,36 @@ def test_modp2048_constant_from_its_definition():
     assert p == sake.MODP2048_P and sake.MODP2048.g == 2
 
 
-def test_rfc4493_cmac_vector():
-    """AES-CMAC K = 2b7e1516..., empty message -> bb1d6929e95937287fa37d129b756746."""
-    c = cmac.CMAC(algorithms.AES(bytes.fromhex("2b7e151628aed2a6abf7158809cf4f3c")))
-    c.update(b"")
-    assert c.finalize().hex() == "bb1d6929e95937287fa37d129b756746"
+RFC4493_KEY = bytes.fromhex("2b7e151628aed2a6abf7158809cf4f3c")
+RFC4493_MSG = bytes.fromhex("6bc1bee22e409f96e93d7e117393172aae2d8a571e03ac9c9eb76fac45af8e51"
+                            "30c81c46a35ce411e5fbc1191a0a52eff69f2445df4f9b17ad2b417be66c3710")
+
+
+@pytest.mark.parametrize("mlen,tag", [(0, "bb1d6929e95937287fa37d129b756746"),
+                                      (16, "070a16b46b4d4144f79bdd9dd04a287c"),
+                                      (40, "dfa66747de9ae63030ca32611497c827"),
+                                      (64, "51f0bebf7e3b9d92fc49741779363cfe")])
+def test_rfc4493_cmac_vectors(mlen, tag):
+    """S:358 / RFC 4493 section 4: AES-CMAC examples 1-4 under K = 2b7e1516..., through
+    the MAC primitive sake.mac uses (empty, one block, a partial last block, four blocks)."""
+    assert sake.cmac_aes128(RFC4493_KEY, RFC4493_MSG[:mlen]).hex() == tag
+
+
+def test_sake_mac_key_derivation_and_check():
+    """sake.mac(km, m) is AES-CMAC under SHA-256(km)[0:16]: the derived key is the
+    hashlib digest prefix, the tag equals the RFC 4493 primitive's under that key, mac_ok
+    accepts it and rejects any single-bit change of tag, message or key material."""
+    km, m = b"session key material", RFC4493_MSG[:40]
+    assert sake.mac_key(km) == hashlib.sha256(km).digest()[:16]
+    tag = sake.mac(km, m)
+    assert tag == sake.cmac_aes128(hashlib.sha256(km).digest()[:16], m)
+    assert sake.mac_ok(km, m, tag)
+    for bit in range(0, 128, 7):
+        bad = bytearray(tag)
+        bad[bit // 8] ^= 1 << (bit % 8)
+        assert not sake.mac_ok(km, m, bytes(bad))
+    assert not sake.mac_ok(km, m[:-1] + bytes([m[-1] ^ 1]), tag)
+    assert not sake.mac_ok(km + b"!", m, tag)
 
 
 def test_toy_group_key_agreement():
