@@ -33,6 +33,16 @@
  * Threads: every function may be called from any thread; calls on the same
  * context are serialised by a per-context lock (use one context per thread or
  * stream for concurrency).  The launch-count read is unsynchronised.
+ *
+ * Device: every function makes the context's device current for the call and
+ * restores the caller's current device before returning.
+ *
+ * Stream ordering: work is enqueued on the config's stream, or -- stream NULL --
+ * on a context-owned BLOCKING stream (cudaStreamDefault flags), which is ordered
+ * with the legacy default stream: device buffers written on the legacy default
+ * stream (plain CUDA calls, torch's default stream) before a call are complete
+ * when the kernel reads them.  With a caller-supplied stream the caller orders its
+ * own work (e.g. zeroes raw_out on that stream, see sage_attest_async).
  */
 #ifndef SAGE_H
 #define SAGE_H
@@ -102,28 +112,45 @@ typedef struct {
     uint32_t ilp_smem;         /* lane states per thread of that SMEM kernel (1 or 2) */
 } sage_info;
 
-/* Create a context on cfg->device.  cfg may be NULL (all defaults).
+/* Initialise the verification function on cfg->device ("Initialization of the
+ * VF": the GPU allocates the VF's buffers before the verifier starts
+ * challenging it).  The default grid occupies every SM with all its threads and
+ * registers, 2 x SMs x 1024 threads, the B200 analogue of the A100's
+ * 2 x 108 x 1024.  cfg may be NULL
+ * (all defaults).  Allocates the 32-byte device result and its pinned host copy,
+ * creates the stream if cfg->stream is NULL, and sets the dynamic shared-memory
+ * limits of the kernels the context can stage into (the only kernel-attribute
+ * change the library makes).  *out is owned by the caller; free it with
+ * sage_checksum_destroy.
  * SAGE_EINVAL: threads % 32 != 0 or > 1024, pick_words not in {1,4,8},
- *              placement unknown, out NULL.  SAGE_ECUDA / SAGE_ENOMEM. */
+ *              placement unknown, device ordinal out of range, out NULL.
+ * SAGE_ENOMEM / SAGE_ECUDA: allocation or runtime failure (nothing is leaked). */
 int sage_checksum_init(const sage_config* cfg, sage_ctx** out);
 
-/* Synchronous attestation over a DEVICE region (SCS-2 with base = region).
- * region_bytes = 4 * P * Nc with Nc a power of two (<= 2^32); region 16-byte
- * aligned (32-byte for P = 8); rounds < 2^32.  Returns when the result is on
- * the host.  SAGE_EINVAL on a violated precondition or NULL pointer;
+/* One attestation, synchronous (the verifier's challenge -> checksum exchange,
+ * P:313-316; the checksum function P:369-463 with the loop of P:638-655 as
+ * SCS-2, base = region).  The host time from before the
+ * launch to the result on the host is out->elapsed_ns, the verifier's t1 - t0
+ * (P:501).
+ * region: DEVICE pointer (borrowed, read-only, must stay unmodified until the
+ * call returns); region_bytes = 4 * P * Nc with Nc a power of two (<= 2^32);
+ * region 16-byte aligned (32-byte for P = 8); rounds < 2^32 (R = 0 is allowed:
+ * the seeded state is folded directly).  Returns when the result is on the host.
+ * SAGE_EINVAL on a violated precondition or NULL pointer;
  * SAGE_EUNSUPPORTED when SAGE_SMEM was forced and the region does not fit, or
  * SAGE_HYBRID was forced without its geometry (see SAGE_HYBRID). */
 int sage_attest(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
                 uint64_t rounds, sage_result* out);
 
-/* As sage_attest, and also writes the per-warp partial sums (n/32 u64, device
- * pointer, warp w = threads 32w..32w+31) so large configs can be checked on
+/* As sage_attest, and also writes the per-warp partial sums of the epilog's
+ * pairwise sum: n/32 u64 to per_warp_out (DEVICE pointer, may be
+ * NULL; warp w = logical threads 32w..32w+31), so large configs can be checked on
  * sampled warps: sum of partials == checksum (mod 2^64). */
 int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
                       uint64_t rounds, uint64_t* per_warp_out, sage_result* out);
 
-/* Asynchronous form: validates, then enqueues the checksum kernel on the
- * context's stream and returns.  raw_out is a DEVICE buffer of 4 u64 that the
+/* Asynchronous form of sage_attest (same operation):
+ * validates, then enqueues the checksum kernel on the context's stream and returns.  raw_out is a DEVICE buffer of 4 u64 that the
  * kernel accumulates into and that the CALLER must zero (on the same stream)
  * before the launch:
  *   raw_out[0] checksum, [1] max CTA cycles, [2] ~(first CTA start ns),
@@ -132,7 +159,7 @@ int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
 int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t region_bytes,
                       uint64_t rounds, uint64_t* raw_out, uint64_t* per_warp_out);
 
-/* Inclusion experiment: as sage_attest with GLOBAL placement,
+/* Inclusion experiment (SAGE section 7.3): as sage_attest with GLOBAL placement,
  * and also counts how often each chunk is read.  counts_out: DEVICE buffer of
  * Nc = region_bytes / (4 * P) u32, zeroed by the call.  The checksum is the
  * same as sage_attest's for the same inputs; the timing is not representative
@@ -150,25 +177,41 @@ int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size
 int sage_kernel_hash(sage_ctx* ctx, const uint8_t* r, size_t r_len, const void* code, size_t code_len,
                      uint8_t* h_out, uint64_t* elapsed_ns);
 
-/* Decode a raw 4 x u64 result (host copy) into checksum / cycles / device_ns. */
+/* Decode a raw 4 x u64 result (host copy of sage_attest_async's raw_out) into
+ * checksum / cycles / device_ns (P:501 timing fields); SAGE_EINVAL on NULL. */
 int sage_decode_raw(const uint64_t raw[4], sage_result* out);
 
-/* End-to-end form over a HOST region: copies the region host->device into a
- * context-owned device buffer (whose VA is reported in out->region_va and is
- * the SCS-2 base), attests, copies the 32-byte result back.  elapsed_ns covers
- * the copies.  Pinned host memory gives the fastest copy. */
+/* End-to-end form of sage_attest over a HOST region (P:313-316 with the region
+ * supplied by the host): copies the region host->device into a context-owned
+ * device buffer (whose VA is reported in out->region_va and is the SCS-2 base),
+ * attests, copies the 32-byte result back.  elapsed_ns covers the copies.
+ * Pinned host memory gives the fastest copy.  region_bytes and rounds are
+ * validated BEFORE the staging buffer is (re)allocated, so an invalid call
+ * (SAGE_EINVAL) leaves the buffer and its VA unchanged; a larger valid region
+ * reallocates it (new VA). */
 int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, size_t region_bytes,
                      uint64_t rounds, sage_result* out);
 
 /* Device VA of the context-owned staging buffer sage_attest_host would use
  * for a region of region_bytes (allocating it if needed), so a verifier can
- * precompute the expected checksum ahead of time. */
+ * precompute the expected checksum ahead of time (the result depends
+ * on the data pointer).  SAGE_EINVAL for an invalid region_bytes. */
 int sage_host_region_va(sage_ctx* ctx, size_t region_bytes, uint64_t* va_out);
 
 /* Placement the context would choose for region_bytes (SAGE_SMEM/SAGE_GLOBAL/SAGE_HYBRID;
  * a HYBRID region whose chunk addresses straddle a 4 GiB boundary runs GLOBAL). */
 int sage_placement_for(sage_ctx* ctx, size_t region_bytes, uint32_t* placement_out);
 
+/* Mangled symbol of the checksum kernel an attestation of region_bytes at device
+ * VA region_va would launch (region_va only decides whether chunk addresses
+ * straddle a 4 GiB boundary; 0 = a region that does not), NUL-terminated into
+ * buf[buf_len].  Lets a verifier place the running kernel's own machine code in
+ * the checksummed region (self-verification; "the beginning of the
+ * buffer contains the checksum function itself").  SAGE_EINVAL: invalid
+ * region_bytes, NULL buf, buf too small; SAGE_EUNSUPPORTED as for sage_attest. */
+int sage_kernel_symbol(sage_ctx* ctx, uint64_t region_va, size_t region_bytes, char* buf, size_t buf_len);
+
+/* Context and kernel facts (read-only: changes no kernel attribute). */
 int sage_query(sage_ctx* ctx, sage_info* out);
 
 /* Number of checksum-kernel launches this context has issued. */

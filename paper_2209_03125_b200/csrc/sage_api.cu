@@ -156,10 +156,36 @@ struct sage_ctx {
 
 namespace {
 
-int set_device(const sage_ctx* c) {
-    CUDA_TRY(cudaSetDevice(c->device));
-    return SAGE_OK;
-}
+// Makes the context's device current for the duration of an entry point and
+// restores the caller's current device on every return path (a torch user on
+// cuda:1 calling into a context on device 0 keeps cuda:1 current).
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) {
+            cudaGetLastError();
+            prev_ = -1;
+        }
+        if (prev_ == device) return;
+        const cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) {
+            rc_ = cuda_fail(e, "cudaSetDevice");
+            return;
+        }
+        restore_ = prev_ >= 0;
+    }
+    ~DeviceGuard() {
+        if (restore_) cudaSetDevice(prev_);
+    }
+    int rc() const { return rc_; }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+  private:
+    int prev_ = -1;
+    bool restore_ = false;
+    int rc_ = SAGE_OK;
+};
 
 // A buffer the kernel dereferences must be device memory the context's device can
 // read: an unregistered host pointer (or another GPU's allocation) would otherwise
@@ -181,20 +207,28 @@ int check_device_ptr(const sage_ctx* c, const void* p, const char* what) {
     return SAGE_OK;
 }
 
-// Check the SCS-2 preconditions on (region, bytes, rounds) for P.
-int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t rounds) {
+// Check the SCS-2 preconditions on (bytes, rounds) for P (no pointer involved).
+int validate_sizes(const sage_ctx* c, size_t bytes, uint64_t rounds) {
     if (c == nullptr) return fail(SAGE_EINVAL, "null context%s");
-    if (region == nullptr) return fail(SAGE_EINVAL, "null region%s");
     const uint64_t P = c->pick_words;
     if (bytes == 0 || bytes % (4 * P) != 0)
         return fail(SAGE_EINVAL, "region_bytes must be a positive multiple of 4*P%s");
     const uint64_t nc = bytes / (4 * P);
     if ((nc & (nc - 1)) != 0 || nc > (1ull << 32))
         return fail(SAGE_EINVAL, "region chunk count must be a power of two <= 2^32%s");
+    if (rounds > 0xFFFFFFFFull) return fail(SAGE_EINVAL, "rounds must be < 2^32%s");
+    return SAGE_OK;
+}
+
+// Check the SCS-2 preconditions on (region, bytes, rounds) for P.
+int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t rounds) {
+    int rc = validate_sizes(c, bytes, rounds);
+    if (rc) return rc;
+    if (region == nullptr) return fail(SAGE_EINVAL, "null region%s");
+    const uint64_t P = c->pick_words;
     const uint64_t align = (4 * P > 16) ? 4 * P : 16;
     if (reinterpret_cast<uintptr_t>(region) % align != 0)
         return fail(SAGE_EINVAL, "region must be 16-byte aligned (32-byte for P=8)%s");
-    if (rounds > 0xFFFFFFFFull) return fail(SAGE_EINVAL, "rounds must be < 2^32%s");
     return check_device_ptr(c, region, "region");
 }
 
@@ -233,9 +267,18 @@ int ensure_dyn_smem(int device, KernelFn fn, int bytes, bool force = false) {
     return SAGE_OK;
 }
 
-int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
-           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
-    uint32_t placement = counts ? SAGE_GLOBAL : choose_placement(c, bytes);
+// The kernel one attestation of (region, bytes) runs: placement, lane states per
+// thread, instantiation and the shared-memory bytes it stages.  region is only used
+// for its address (the 4 GiB straddle test), never dereferenced.
+struct Plan {
+    KernelFn fn = nullptr;
+    uint32_t placement = SAGE_GLOBAL;
+    uint32_t ilp = 1;
+    size_t dyn = 0;
+};
+
+int plan_launch(const sage_ctx* c, const void* region, size_t bytes, bool counting, Plan* out) {
+    uint32_t placement = counting ? SAGE_GLOBAL : choose_placement(c, bytes);
     if (placement == SAGE_SMEM && bytes > smem_region_max(c))
         return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s",
                     hybrid_geometry(c) ? "128 KiB" : "64 KiB");
@@ -256,13 +299,28 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     }
     const bool hybrid = placement == SAGE_HYBRID;
     const bool smem = placement == SAGE_SMEM;
-    uint32_t ilp = counts ? 1 : ilp_for(c->pick_words, smem, straddle, c->blocks, c->threads);
-    KernelFn fn = counts ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle, ilp);
+    uint32_t ilp = counting ? 1 : ilp_for(c->pick_words, smem, straddle, c->blocks, c->threads);
+    KernelFn fn = counting ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle, ilp);
     if (hybrid) {
         ilp = kIlpSmem;
         fn = hybrid_kernel();
     }
-    const size_t dyn = smem ? bytes : hybrid ? (bytes < kHybridStage ? bytes : kHybridStage) : 0;
+    if (fn == nullptr) return fail(SAGE_EINVAL, "pick_words must be 1, 4 or 8%s");
+    out->fn = fn;
+    out->placement = placement;
+    out->ilp = ilp;
+    out->dyn = smem ? bytes : hybrid ? (bytes < kHybridStage ? bytes : kHybridStage) : 0;
+    return SAGE_OK;
+}
+
+int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
+           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
+    Plan plan;
+    int prc = plan_launch(c, region, bytes, counts != nullptr, &plan);
+    if (prc) return prc;
+    const KernelFn fn = plan.fn;
+    const uint32_t placement = plan.placement, ilp = plan.ilp;
+    const size_t dyn = plan.dyn;
     if (dyn) {
         int rc = ensure_dyn_smem(c->device, fn, static_cast<int>(dyn));
         if (rc) return rc;
@@ -305,16 +363,14 @@ void fill_result(const sage_ctx* c, const uint64_t raw[4], uint64_t t0, uint64_t
     out->pick_words = c->pick_words;
 }
 
-// attest synchronously over a device region already validated
+// attest synchronously over a device region already validated (device already current)
 int attest_device(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds,
                   uint64_t* per_warp, sage_result* out, const void* host_src, uint32_t* counts = nullptr) {
-    int rc = set_device(c);
-    if (rc) return rc;
     const uint64_t t0 = now_ns();
     if (host_src) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(region), host_src, bytes, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_raw, 0, 4 * sizeof(uint64_t), c->stream));
     uint32_t placement = 0, ilp = 1;
-    rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts, &ilp);
+    int rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts, &ilp);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->h_raw, c->d_raw, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -334,6 +390,18 @@ int ensure_stage(sage_ctx* c, size_t bytes) {
     return SAGE_OK;
 }
 
+// Dynamic shared-memory limits of the kernels this context can stage into, set
+// once when the context is created so that later calls (sage_query, launches)
+// do not change kernel attributes.
+int prepare_kernels(const sage_ctx* c) {
+    const uint32_t ilp = ilp_for(c->pick_words, true, false, c->blocks, c->threads);
+    int rc = ensure_dyn_smem(c->device, kernel_for(c->pick_words, true, false, ilp),
+                             static_cast<int>(smem_region_max(c)));
+    if (rc == SAGE_OK) rc = ensure_dyn_smem(c->device, kernel_for(c->pick_words, true, true), static_cast<int>(kSmemRegionMax));
+    if (rc == SAGE_OK && hybrid_geometry(c)) rc = ensure_dyn_smem(c->device, hybrid_kernel(), static_cast<int>(kHybridStage));
+    return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -351,7 +419,8 @@ int sage_checksum_init(const sage_config* cfg, sage_ctx** out) {
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (d.device < 0 || d.device >= ndev) return fail(SAGE_EINVAL, "device ordinal out of range%s");
-    CUDA_TRY(cudaSetDevice(d.device));
+    DeviceGuard dg(d.device);
+    if (dg.rc()) return dg.rc();
     int sms = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
 
@@ -367,7 +436,10 @@ int sage_checksum_init(const sage_config* cfg, sage_ctx** out) {
     if (d.stream) {
         c->stream = static_cast<cudaStream_t>(d.stream);
     } else {
-        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        // a blocking stream: its work is ordered with the legacy default stream (the one
+        // torch and plain CUDA code use unless told otherwise), so buffers written there
+        // before an attestation call are complete when the kernel reads them
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault);
         if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaStreamCreate"); }
         c->own_stream = true;
     }
@@ -375,6 +447,8 @@ int sage_checksum_init(const sage_config* cfg, sage_ctx** out) {
     if (e != cudaSuccess) { sage_checksum_destroy(c); return fail(SAGE_ENOMEM, "cudaMalloc result%s"); }
     e = cudaMallocHost(&c->h_raw, 4 * sizeof(uint64_t));
     if (e != cudaSuccess) { sage_checksum_destroy(c); return fail(SAGE_ENOMEM, "cudaMallocHost result%s"); }
+    const int rc = prepare_kernels(c);
+    if (rc) { sage_checksum_destroy(c); return rc; }
     *out = c;
     return SAGE_OK;
 }
@@ -392,6 +466,8 @@ int sage_attest_debug(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     rc = check_device_ptr(ctx, per_warp_out, "per_warp_out");
     if (rc) return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
     sage_result tmp;
     rc = attest_device(ctx, nonce, region, region_bytes, rounds, per_warp_out, &tmp, nullptr);
     if (rc) return rc;
@@ -407,8 +483,8 @@ int sage_attest_async(sage_ctx* ctx, uint64_t nonce, const void* region, size_t 
     if ((rc = check_device_ptr(ctx, raw_out, "raw_out")) || (rc = check_device_ptr(ctx, per_warp_out, "per_warp_out")))
         return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
-    rc = set_device(ctx);
-    if (rc) return rc;
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
     return launch(ctx, nonce, region, region_bytes, rounds, raw_out, per_warp_out, nullptr);
 }
 
@@ -420,8 +496,8 @@ int sage_attest_coverage(sage_ctx* ctx, uint64_t nonce, const void* region, size
     rc = check_device_ptr(ctx, counts_out, "counts_out");
     if (rc) return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
-    rc = set_device(ctx);
-    if (rc) return rc;
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
     CUDA_TRY(cudaMemsetAsync(counts_out, 0, region_bytes / (4ull * ctx->pick_words) * sizeof(uint32_t), ctx->stream));
     sage_result tmp;
     rc = attest_device(ctx, nonce, region, region_bytes, rounds, nullptr, &tmp, nullptr, counts_out);
@@ -440,8 +516,8 @@ int sage_kernel_hash(sage_ctx* ctx, const uint8_t* r, size_t r_len, const void* 
         if (rc) return rc;
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
-    int rc = set_device(ctx);
-    if (rc) return rc;
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
     sage::HashArgs args{};
     args.code = static_cast<const uint8_t*>(code);
     args.code_len = code_len;
@@ -473,10 +549,14 @@ int sage_decode_raw(const uint64_t raw[4], sage_result* out) {
 int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, size_t region_bytes, uint64_t rounds,
                      sage_result* out) {
     if (ctx == nullptr || host_region == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
-    std::lock_guard<std::mutex> lock(ctx->mu);
-    int rc = set_device(ctx);
+    // sizes first: an invalid call must not reallocate the staging buffer (its VA is
+    // what a verifier precomputed the expected checksum for, sage_host_region_va)
+    int rc = validate_sizes(ctx, region_bytes, rounds);
     if (rc) return rc;
-    rc = ensure_stage(ctx, region_bytes ? region_bytes : 1);
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
+    rc = ensure_stage(ctx, region_bytes);
     if (rc) return rc;
     rc = validate(ctx, ctx->d_stage, region_bytes, rounds);
     if (rc) return rc;
@@ -489,10 +569,12 @@ int sage_attest_host(sage_ctx* ctx, uint64_t nonce, const void* host_region, siz
 
 int sage_host_region_va(sage_ctx* ctx, size_t region_bytes, uint64_t* va_out) {
     if (ctx == nullptr || va_out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
-    std::lock_guard<std::mutex> lock(ctx->mu);
-    int rc = set_device(ctx);
+    int rc = validate_sizes(ctx, region_bytes, 0);
     if (rc) return rc;
-    rc = ensure_stage(ctx, region_bytes ? region_bytes : 1);
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
+    rc = ensure_stage(ctx, region_bytes);
     if (rc) return rc;
     *va_out = reinterpret_cast<uint64_t>(ctx->d_stage);
     return SAGE_OK;
@@ -504,10 +586,27 @@ int sage_placement_for(sage_ctx* ctx, size_t region_bytes, uint32_t* placement_o
     return SAGE_OK;
 }
 
+int sage_kernel_symbol(sage_ctx* ctx, uint64_t region_va, size_t region_bytes, char* buf, size_t buf_len) {
+    if (ctx == nullptr || buf == nullptr || buf_len == 0) return fail(SAGE_EINVAL, "null pointer%s");
+    int rc = validate_sizes(ctx, region_bytes, 0);
+    if (rc) return rc;
+    Plan plan;
+    rc = plan_launch(ctx, reinterpret_cast<const void*>(region_va), region_bytes, false, &plan);
+    if (rc) return rc;
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
+    const char* name = nullptr;
+    CUDA_TRY(cudaFuncGetName(&name, reinterpret_cast<const void*>(plan.fn)));
+    const size_t n = strlen(name);
+    if (n + 1 > buf_len) return fail(SAGE_EINVAL, "buffer too small for the kernel symbol%s");
+    memcpy(buf, name, n + 1);
+    return SAGE_OK;
+}
+
 int sage_query(sage_ctx* ctx, sage_info* out) {
     if (ctx == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
-    int rc = set_device(ctx);
-    if (rc) return rc;
+    DeviceGuard dg(ctx->device);
+    if (dg.rc()) return dg.rc();
     sage_info info{};
     info.device = ctx->device;
     info.sm_count = ctx->sm_count;
@@ -518,9 +617,8 @@ int sage_query(sage_ctx* ctx, sage_info* out) {
     info.smem_region_max = smem_region_max(ctx);
     const uint32_t ilp = ilp_for(ctx->pick_words, true, false, ctx->blocks, ctx->threads);
     info.ilp_smem = ilp;
+    // read-only: the dynamic shared-memory limit of the SMEM kernel was set at init
     KernelFn fs = kernel_for(ctx->pick_words, true, false, ilp), fg = kernel_for(ctx->pick_words, false, true);
-    rc = ensure_dyn_smem(ctx->device, fs, static_cast<int>(kSmemRegionMax));
-    if (rc) return rc;
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs, static_cast<int>(ctx->threads), kSmemRegionMax));
     info.ctas_per_sm_smem = static_cast<uint32_t>(occ);
@@ -539,7 +637,7 @@ void* sage_stream(const sage_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st
 
 void sage_checksum_destroy(sage_ctx* ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
+    DeviceGuard dg(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->d_raw) cudaFree(ctx->d_raw);
     if (ctx->h_raw) cudaFreeHost(ctx->h_raw);

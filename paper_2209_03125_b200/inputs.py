@@ -37,22 +37,34 @@ def _elf_sections(blob):
     return out
 
 
-def kernel_code_prefix(pick_words=1, smem=True):
-    """Machine code (SASS) of the checksum kernel variant itself, taken from the
-    .text section of the cubin the build writes next to libsage.so; b'' when it
-    has not been built.  Used as the region prefix so the checksummed region
-    carries the checksum function's own instructions (self-verification,
-    P:370-381; buffer layout P:365-367)."""
+def kernel_text(symbol):
+    """Machine code (SASS) of one checksum kernel: the .text section of `symbol` in
+    the cubin the build writes next to libsage.so (compiled from the same source
+    with the same flags); b'' when it has not been built."""
     path = os.path.join(_PKG, "sage_kernel.cubin")
     if not os.path.exists(path):
         return b""
     with open(path, "rb") as f:
         secs = _elf_sections(f.read())
-    want = ".text._ZN4sage20sage_checksum_kernelILi%dELb%d" % (pick_words, 1 if smem else 0)
-    for name, data in sorted(secs.items()):
-        if name.startswith(want):
-            return bytes(data)
-    return b""
+    return bytes(secs.get(".text." + symbol, b""))
+
+
+def kernel_code_prefix(ctx, nbytes, region_va=0):
+    """Region prefix for a self-verifying attestation: the machine code of the very
+    kernel an attestation of nbytes (at region_va) on context ctx launches
+    (ctx.kernel_symbol asks the library which instantiation it picks), so the
+    checksummed region carries the running checksum function's own instructions
+    (self-verification; "the beginning of the buffer contains the
+    checksum function itself")."""
+    return kernel_text(ctx.kernel_symbol(nbytes, region_va))
+
+
+def launched_kernel_prefix(nbytes, region_va=0, device=0, **cfg):
+    """kernel_code_prefix for a context of configuration cfg (sage.Context keyword
+    arguments: blocks, threads, pick_words, placement), created just to ask."""
+    from .sage import Context
+    with Context(device=device, **cfg) as ctx:
+        return kernel_code_prefix(ctx, nbytes, region_va)
 
 
 def make_region(nbytes, fill_seed=REGION_FILL_SEED, prefix=b""):

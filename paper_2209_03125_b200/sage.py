@@ -22,7 +22,7 @@ PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto", 
 # every symbol include/sage.h declares
 EXPORTS = ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
            "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va",
-           "sage_placement_for", "sage_query", "sage_launch_count", "sage_stream", "sage_checksum_destroy",
+           "sage_placement_for", "sage_kernel_symbol", "sage_query", "sage_launch_count", "sage_stream", "sage_checksum_destroy",
            "sage_strerror", "sage_last_error")
 
 
@@ -80,6 +80,7 @@ def load(path=LIB):
     L.sage_attest_host.argtypes = [p, u64, p, sz, u64, ctypes.POINTER(sage_result)]
     L.sage_host_region_va.argtypes = [p, sz, ctypes.POINTER(u64)]
     L.sage_placement_for.argtypes = [p, sz, ctypes.POINTER(ctypes.c_uint32)]
+    L.sage_kernel_symbol.argtypes = [p, u64, sz, ctypes.c_char_p, sz]
     L.sage_query.argtypes = [p, ctypes.POINTER(sage_info)]
     L.sage_launch_count.argtypes = [p]
     L.sage_launch_count.restype = u64
@@ -93,7 +94,7 @@ def load(path=LIB):
     L.sage_last_error.restype = ctypes.c_char_p
     for name in ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
                  "sage_attest_coverage", "sage_kernel_hash", "sage_attest_host", "sage_host_region_va",
-                 "sage_placement_for", "sage_query"):
+                 "sage_placement_for", "sage_kernel_symbol", "sage_query"):
         getattr(L, name).restype = i
     _lib = L
     return L
@@ -215,6 +216,14 @@ def placement_for(ctx, nbytes):
     return pl.value
 
 
+def kernel_symbol(ctx, nbytes, region_va=0):
+    """Mangled name of the checksum kernel an attestation of nbytes at region_va
+    (0: a region not straddling a 4 GiB boundary) would launch."""
+    buf = ctypes.create_string_buffer(512)
+    _check(load().sage_kernel_symbol(ctx, int(region_va), int(nbytes), buf, len(buf)))
+    return buf.value.decode()
+
+
 def query(ctx):
     info = sage_info()
     _check(load().sage_query(ctx, ctypes.byref(info)))
@@ -271,6 +280,9 @@ class Context:
 
     def placement_for(self, nbytes):
         return placement_for(self.ctx, nbytes)
+
+    def kernel_symbol(self, nbytes, region_va=0):
+        return kernel_symbol(self.ctx, nbytes, region_va)
 
     def query(self):
         return query(self.ctx)

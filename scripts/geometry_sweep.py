@@ -4,8 +4,8 @@ fastest (dev aid)."""
 import torch, time, sys
 sys.path.insert(0, '.')
 from paper_2209_03125_b200 import sage
-from paper_2209_03125_b200.inputs import make_region, kernel_code_prefix
-region = torch.from_numpy(make_region(8192, prefix=kernel_code_prefix(1, True))).to('cuda')
+from paper_2209_03125_b200.inputs import make_region, launched_kernel_prefix
+region = torch.from_numpy(make_region(8192, prefix=launched_kernel_prefix(8192))).to('cuda')
 s = torch.cuda.Stream()
 for threads in (1024, 512, 256, 128):
     blocks = 303104 // threads

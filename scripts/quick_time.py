@@ -9,13 +9,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2209_03125_b200 import sage  # noqa: E402
-from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region  # noqa: E402
+from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region  # noqa: E402
 
 
 def time_cfg(nbytes, P, R, reps=5, placement=sage.SAGE_AUTO):
     dev = torch.device("cuda:0")
     if nbytes <= (1 << 20):
-        region = torch.from_numpy(make_region(nbytes, prefix=kernel_code_prefix(P, True))).to(dev)
+        region = torch.from_numpy(make_region(nbytes, prefix=launched_kernel_prefix(nbytes, pick_words=P))).to(dev)
     else:
         region = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev)
     s = torch.cuda.Stream()

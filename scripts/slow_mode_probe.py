@@ -19,7 +19,7 @@ import pynvml  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2209_03125_b200 import sage  # noqa: E402
-from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces  # noqa: E402
+from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, nonces  # noqa: E402
 
 POLICIES = {name: getattr(pynvml, "NVML_PERF_POLICY_" + name) for name in
             ("POWER", "THERMAL", "SYNC_BOOST", "BOARD_LIMIT", "LOW_UTILIZATION", "RELIABILITY",
@@ -45,7 +45,7 @@ def main():
     a = ap.parse_args()
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
-    region = torch.from_numpy(make_region(8192, prefix=kernel_code_prefix(1, True))).to("cuda")
+    region = torch.from_numpy(make_region(8192, prefix=launched_kernel_prefix(8192))).to("cuda")
     runs = []
     with sage.Context() as ctx:
         ns = nonces(a.runs + 3, master_seed=0x51070)

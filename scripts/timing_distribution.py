@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2209_03125_b200 import sage, verifier  # noqa: E402
-from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces  # noqa: E402
+from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, nonces  # noqa: E402
 
 M64 = (1 << 64) - 1
 
@@ -45,7 +45,7 @@ def moments(xs):
 
 def run(rounds_list, counts, samples_per_r, out):
     dev = torch.device("cuda:0")
-    region_np = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region_np = make_region(8192, prefix=launched_kernel_prefix(8192))
     region = torch.from_numpy(region_np).to(dev)
     stream = torch.cuda.Stream()
     result = {"what": "SAGE attestation-time distribution (config 4)", "gpu": torch.cuda.get_device_name(0),

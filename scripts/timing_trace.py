@@ -19,7 +19,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2209_03125_b200 import sage  # noqa: E402
-from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces  # noqa: E402
+from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, nonces  # noqa: E402
 
 Q = ("timestamp,clocks.sm,clocks.mem,power.draw,temperature.gpu,clocks_event_reasons.active,"
      "clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -43,7 +43,7 @@ def main():
     th = threading.Thread(target=rd, daemon=True)
     th.start()
     dev = torch.device("cuda:0")
-    region = torch.from_numpy(make_region(8192, prefix=kernel_code_prefix(1, True))).to(dev)
+    region = torch.from_numpy(make_region(8192, prefix=launched_kernel_prefix(8192))).to(dev)
     runs = []
     with sage.Context() as ctx:
         ns = nonces(a.runs + 3, master_seed=0x7ACE)

@@ -89,6 +89,7 @@ def test_null_context_is_rejected_without_device(lib):
              lambda: sage.attest_host(None, 0, np.zeros(16, np.uint8), 1),
              lambda: sage.host_region_va(None, 16),
              lambda: sage.placement_for(None, 16),
+             lambda: sage.kernel_symbol(None, 16),
              lambda: sage.query(None),
              lambda: sage.kernel_hash(None, b"", None)]
     for call in calls:

@@ -10,7 +10,7 @@ torch = pytest.importorskip("torch")
 
 import oracle                                                              # noqa: E402
 from paper_2209_03125_b200 import sage                                     # noqa: E402
-from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region, nonces   # noqa: E402
+from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, nonces   # noqa: E402
 
 pytestmark = pytest.mark.gpu
 M64 = (1 << 64) - 1
@@ -19,7 +19,7 @@ M64 = (1 << 64) - 1
 def test_full_occupancy_full_rounds_every_warp():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d = torch.from_numpy(region).to("cuda")
     R = 100_000
     nonce = nonces(2)[1]
@@ -43,7 +43,7 @@ def test_config4_full_result_twenty_nonces():
     sum consistency for the rest, which tests/test_c4_samples.py covers)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d = torch.from_numpy(region).to("cuda")
     R = 10_000
     ns = nonces(22)[2:]

@@ -9,7 +9,7 @@ torch = pytest.importorskip("torch")
 
 import oracle                                                     # noqa: E402
 from paper_2209_03125_b200 import sage                            # noqa: E402
-from paper_2209_03125_b200.inputs import (C1_NONCE, kernel_code_prefix, make_region,  # noqa: E402
+from paper_2209_03125_b200.inputs import (C1_NONCE, launched_kernel_prefix, make_region,  # noqa: E402
                                            nonces)
 
 pytestmark = pytest.mark.gpu
@@ -40,7 +40,7 @@ def to_dev(region_np, dev, align_offset=0):
 
 def test_config1_bit_exact(dev):
     """BASELINE configs[0]: 1 x 32 threads, 4 KiB region, 10^4 rounds, fixed nonce."""
-    region = make_region(4096, prefix=kernel_code_prefix(1, True))
+    region = make_region(4096, prefix=launched_kernel_prefix(4096, blocks=1, threads=32))
     d, _keep = to_dev(region, dev)
     with sage.Context(blocks=1, threads=32) as ctx:
         res = ctx.attest(C1_NONCE, d, 10_000)
@@ -98,7 +98,8 @@ def test_zero_rounds(dev):
 
 @pytest.mark.parametrize("P", [1, 4, 8])
 def test_smem_and_global_placements_agree(dev, P):
-    region = make_region(4 * P * 2048, prefix=kernel_code_prefix(P, True))
+    region = make_region(4 * P * 2048, prefix=launched_kernel_prefix(4 * P * 2048, blocks=4, threads=256, pick_words=P,
+                                                                     placement=sage.SAGE_SMEM))
     d, _keep = to_dev(region, dev)
     out = {}
     for placement in (sage.SAGE_SMEM, sage.SAGE_GLOBAL):
@@ -111,7 +112,7 @@ def test_full_occupancy_repeatable_and_sampled(dev):
     """Full occupancy (2 x SMs x 1024), 8 KiB SMEM region: repeat runs are
     bit-identical (atomic-order independence, Q11), the per-warp partials sum
     to the checksum, and sampled warps match the oracle exactly."""
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d, _keep = to_dev(region, dev)
     R = 2000
     with sage.Context() as ctx:
@@ -132,7 +133,7 @@ def test_full_occupancy_repeatable_and_sampled(dev):
 def test_bench_config_full_rounds_sampled(dev):
     """configs[1] as bench.py times it: full occupancy, 8 KiB SMEM region,
     10^5 rounds; sum consistency plus 4 sampled warps recomputed by the oracle."""
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d, _keep = to_dev(region, dev)
     R = 100_000
     nonce = nonces(1)[0]
@@ -189,7 +190,7 @@ def test_region_straddling_4gib_boundary(dev, P):
 
 def test_largest_smem_region(dev):
     """64 KiB is the largest region staged into SMEM at 2 CTAs/SM."""
-    region = make_region(65536, prefix=kernel_code_prefix(1, True))
+    region = make_region(65536, prefix=launched_kernel_prefix(65536, blocks=3, threads=128))
     d, _keep = to_dev(region, dev)
     with sage.Context(blocks=3, threads=128) as ctx:
         assert ctx.placement_for(65536) == sage.SAGE_SMEM
@@ -200,7 +201,7 @@ def test_largest_smem_region(dev):
 
 
 def test_async_and_host_forms(dev):
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d, _keep = to_dev(region, dev)
     with sage.Context(blocks=2, threads=256) as ctx:
         raw = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -341,7 +342,7 @@ def test_multiple_waves(dev):
 
 
 def test_p8_auto_placement_is_global(dev):
-    region = make_region(8192, prefix=kernel_code_prefix(8, False))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192, blocks=2, threads=96, pick_words=8))
     d, _keep = to_dev(region, dev)
     with sage.Context(blocks=2, threads=96, pick_words=8) as ctx:
         assert ctx.placement_for(8192) == sage.SAGE_GLOBAL
@@ -352,7 +353,7 @@ def test_p8_auto_placement_is_global(dev):
 def test_async_attestation_in_cuda_graph(dev):
     """sage_attest_async is capturable: a CUDA graph of zero-fill + attestation,
     replayed twice, reproduces the synchronous checksum."""
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d, _keep = to_dev(region, dev)
     s = torch.cuda.Stream()
     raw = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -414,7 +415,7 @@ def test_one_context_shared_by_threads(dev):
 def test_full_occupancy_wide_picks_sampled(dev, P):
     """P = 4 (SMEM, 16-B picks) and P = 8 (AUTO -> L1-resident GLOBAL, 32-B picks)
     at full occupancy, 8 KiB region, 10^4 rounds: Σ-consistency + sampled warps."""
-    region = make_region(8192, prefix=kernel_code_prefix(P, P == 4))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192, pick_words=P))
     d, _keep = to_dev(region, dev)
     R = 10_000
     with sage.Context(pick_words=P) as ctx:
@@ -432,7 +433,7 @@ def test_full_occupancy_wide_picks_sampled(dev, P):
 def test_ilp2_smem_region_up_to_128k(dev):
     """At the ILP-2 geometry (one CTA per SM) SAGE_AUTO stages regions up to 128 KiB in
     shared memory; bit-exact with the oracle and with GLOBAL."""
-    region = make_region(128 << 10, prefix=kernel_code_prefix(1, True))
+    region = make_region(128 << 10, prefix=launched_kernel_prefix(128 << 10, blocks=2, threads=1024))
     d, _keep = to_dev(region, dev)
     with sage.Context(blocks=2, threads=1024) as ctx:
         assert ctx.query().smem_region_max == 128 << 10
@@ -454,7 +455,7 @@ def test_hybrid_placement_bit_exact(dev, nbytes):
     """SAGE_HYBRID (first 192 KiB in shared memory, the rest read in place): chosen by
     SAGE_AUTO for 128 KiB < region <= 1 MiB at a 1024-thread, even-block geometry, and
     bit-exact with the oracle and with the GLOBAL placement."""
-    region = make_region(nbytes, prefix=kernel_code_prefix(1, False), fill_seed=nbytes)
+    region = make_region(nbytes, prefix=launched_kernel_prefix(nbytes, blocks=2, threads=1024), fill_seed=nbytes)
     d, _keep = to_dev(region, dev, align_offset=16)
     out = {}
     for placement in (sage.SAGE_AUTO, sage.SAGE_GLOBAL):
@@ -516,7 +517,7 @@ def test_ilp2_placements_straddling_region_run_global(dev, nbytes):
 def test_paper_buffer_full_occupancy_sampled(dev):
     """c2c as bench.py times it: the paper's 524,288-B buffer at full
     occupancy (SAGE_HYBRID), 10^5 rounds; sum consistency plus sampled warps."""
-    region = make_region(512 << 10, prefix=kernel_code_prefix(1, False))
+    region = make_region(512 << 10, prefix=launched_kernel_prefix(512 << 10))
     d, _keep = to_dev(region, dev)
     R = 100_000
     with sage.Context() as ctx:
@@ -567,7 +568,7 @@ def test_relocated_copy_gives_a_different_checksum(dev):
     """The data pointer is folded in every round, so the same bytes
     attested at another device address (a relocated copy of the verification
     function) give a different checksum -- each equal to the oracle's at its own VA."""
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d1, _k1 = to_dev(region, dev)
     d2, _k2 = to_dev(region, dev, align_offset=4096)
     assert d1.data_ptr() != d2.data_ptr()
@@ -584,7 +585,7 @@ def test_single_bit_flips_change_the_gpu_checksum(dev):
     the attestation result; 16 random bits of an 8 KiB region at full occupancy
     with enough rounds that every word is read (R = 64), each result equal to
     the oracle's on the flipped bytes."""
-    region = make_region(8192, prefix=kernel_code_prefix(1, True))
+    region = make_region(8192, prefix=launched_kernel_prefix(8192))
     d, _keep = to_dev(region, dev)
     rng = np.random.default_rng(11)
     with sage.Context() as ctx:
