@@ -54,6 +54,8 @@ def lib():
         L.sage_oracle_sha256.argtypes = [p, u64, p, u64, p]
         L.sage_oracle_attest.restype = ctypes.c_int
         L.sage_oracle_attest.argtypes = [u64, p, u64, u64, u64, u64, u64, ctypes.c_uint, p]
+        L.sage_oracle_attest_counts.restype = ctypes.c_int
+        L.sage_oracle_attest_counts.argtypes = [u64, p, u64, u64, u64, u64, u64, ctypes.c_uint, p, p]
         _lib = L
     return _lib
 
@@ -113,6 +115,19 @@ def attest(nonce, region, base, rounds, blocks, threads, P=1):
     if rc != 0:
         raise ValueError("oracle rejected arguments")
     return out.value
+
+
+def attest_counts(nonce, region, base, rounds, blocks, threads, P=1):
+    """(checksum, per-chunk pick counts as a uint32 array) -- the inclusion
+    experiment counted by the oracle."""
+    arr, ptr, n = _buf(region)
+    counts = np.zeros(n // (4 * P), dtype=np.uint32)
+    out = ctypes.c_uint64(0)
+    rc = lib().sage_oracle_attest_counts(nonce, ptr, n, base, rounds, blocks, threads, P, ctypes.byref(out),
+                                         counts.ctypes.data_as(ctypes.c_void_p))
+    if rc != 0:
+        raise ValueError("oracle rejected arguments")
+    return out.value, counts
 
 
 def sha256(r, code):

@@ -93,7 +93,8 @@ void sage_oracle_thread_init(uint64_t nonce, uint64_t g, uint32_t a[K], uint64_t
 /* ---- one round r for all 32 lanes of a warp (P:638-655 steps 1-5, north_star
  * neighbour exchange).  nc = number of P-word chunks (power of two). -------- */
 static void warp_round(uint32_t a[WARP][K], uint64_t x[WARP], uint32_t r,
-                       const uint8_t *region, uint64_t nc, uint64_t base, unsigned P)
+                       const uint8_t *region, uint64_t nc, uint64_t base, unsigned P,
+                       uint32_t *counts)
 {
     uint32_t t_lane[WARP];
     for (int l = 0; l < WARP; l++) {
@@ -104,6 +105,9 @@ static void warp_round(uint32_t a[WARP][K], uint64_t x[WARP], uint32_t r,
         uint32_t C = a[l][K - 1];
         /* R3: chunk index; 4*C % data_size with power-of-two size (Q1) */
         uint64_t i = (uint64_t)(hi32(y) ^ C) & (nc - 1);
+        /* inclusion experiment: count the pick of chunk i */
+        if (counts != NULL)
+            counts[i] += 1;
         /* R4: pseudo-random read of P consecutive words */
         uint32_t d[8];
         for (unsigned q = 0; q < P; q++)
@@ -165,7 +169,7 @@ int sage_oracle_warp_rounds(uint32_t *a_flat, uint64_t *x, const uint8_t *region
     uint64_t nc = nbytes / (4ULL * P);
     uint32_t (*a)[K] = (uint32_t (*)[K])a_flat;
     for (uint64_t r = r_begin; r < r_end; r++)
-        warp_round(a, x, (uint32_t)r, region, nc, base, P);
+        warp_round(a, x, (uint32_t)r, region, nc, base, P, NULL);
     return 0;
 }
 
@@ -173,8 +177,8 @@ int sage_oracle_warp_rounds(uint32_t *a_flat, uint64_t *x, const uint8_t *region
  * Sum mod 2^64 of the folded states of the 32 threads g = 32*w .. 32*w+31.
  * This is the warp-level partial of the epilog.
  */
-int sage_oracle_warp(uint64_t nonce, const uint8_t *region, uint64_t nbytes, uint64_t base,
-                     uint64_t rounds, uint64_t w, unsigned P, uint64_t *warp_sum)
+static int warp_sum_counted(uint64_t nonce, const uint8_t *region, uint64_t nbytes, uint64_t base,
+                            uint64_t rounds, uint64_t w, unsigned P, uint64_t *warp_sum, uint32_t *counts)
 {
     if (check_args(region, nbytes, base, rounds, P) != 0 || warp_sum == NULL) return -1;
     uint32_t a[WARP][K];
@@ -183,11 +187,37 @@ int sage_oracle_warp(uint64_t nonce, const uint8_t *region, uint64_t nbytes, uin
         sage_oracle_thread_init(nonce, 32ULL * w + (uint64_t)l, a[l], &x[l]);
     uint64_t nc = nbytes / (4ULL * P);
     for (uint64_t r = 0; r < rounds; r++)
-        warp_round(a, x, (uint32_t)r, region, nc, base, P);
+        warp_round(a, x, (uint32_t)r, region, nc, base, P, counts);
     uint64_t sum = 0;
     for (int l = 0; l < WARP; l++)
         sum += sage_oracle_fold(a[l], x[l]);
     *warp_sum = sum;
+    return 0;
+}
+
+int sage_oracle_warp(uint64_t nonce, const uint8_t *region, uint64_t nbytes, uint64_t base,
+                     uint64_t rounds, uint64_t w, unsigned P, uint64_t *warp_sum)
+{
+    return warp_sum_counted(nonce, region, nbytes, base, rounds, w, P, warp_sum, NULL);
+}
+
+/*
+ * Inclusion experiment: as sage_oracle_attest, and also adds to
+ * counts[k] (Nc u32, caller-zeroed) the number of times chunk k is picked.
+ */
+int sage_oracle_attest_counts(uint64_t nonce, const uint8_t *region, uint64_t nbytes, uint64_t base,
+                              uint64_t rounds, uint64_t blocks, uint64_t threads, unsigned P,
+                              uint64_t *checksum, uint32_t *counts)
+{
+    if (checksum == NULL || counts == NULL || threads == 0 || threads % WARP != 0 || blocks == 0) return -1;
+    uint64_t nwarps = blocks * threads / WARP;
+    uint64_t total = 0;
+    for (uint64_t w = 0; w < nwarps; w++) {
+        uint64_t s;
+        if (warp_sum_counted(nonce, region, nbytes, base, rounds, w, P, &s, counts) != 0) return -1;
+        total += s;
+    }
+    *checksum = total;
     return 0;
 }
 

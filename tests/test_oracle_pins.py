@@ -557,3 +557,32 @@ def test_exchange_multiplier_is_a_permutation():
         A[0, 15] = v
         out = int(run(A, X0, 0x4000, 9)[0, 15])
         assert ((out - ref) * Kinv) & M32 == v, v
+
+
+# ------------------------------------------------ R3 read-count instrumentation
+def test_pick_counts_config1_read_every_word():
+    """SURVEY 8(c) R3 pin: at config 1 (1 x 32 threads, 1,024 words, 10^4 rounds =
+    3.2 x 10^5 picks) every word is read -- under uniform picks each word is missed
+    with probability (1 - 1/1024)^320000 ~ e^-312.5 -- the counts add up to the
+    number of picks, and instrumenting does not change the checksum."""
+    region = np.random.default_rng(1).integers(0, 256, 4096, dtype=np.uint8)
+    cs, counts = oracle.attest_counts(0x0123456789ABCDEF, region, 0x7F00_0000_0000, 10_000, 1, 32, 1)
+    assert cs == oracle.attest(0x0123456789ABCDEF, region, 0x7F00_0000_0000, 10_000, 1, 32, 1)
+    assert int(counts.sum()) == 32 * 10_000 and int(counts.min()) > 0
+    # uniform picks: each count is Binomial(N, 1/1024); chi-square over the 1,024 words
+    e = 32 * 10_000 / 1024
+    chi2 = float(((counts - e) ** 2 / e).sum())
+    assert chi2 < 1023 + 6 * (2 * 1023) ** 0.5, chi2
+
+
+def test_pick_counts_follow_the_inclusion_formula():
+    """P:747-749 with the formula of S:302: N = 100,000 picks over S = 131,072 words
+    leave a fraction (1 - 1/S)^N = 0.4663 unread (within 6 standard errors)."""
+    S, rounds = 131072, 3125
+    region = np.random.default_rng(2).integers(0, 256, 4 * S, dtype=np.uint8)
+    _, counts = oracle.attest_counts(77, region, 0x10000, rounds, 1, 32, 1)
+    N = 32 * rounds
+    p = (1 - 1 / S) ** N
+    unread = float((counts == 0).mean())
+    assert abs(p - 0.46629) < 1e-4
+    assert abs(unread - p) < 6 * (p * (1 - p) / S) ** 0.5, (unread, p)
