@@ -103,7 +103,19 @@ __global__ void __launch_bounds__(1024, 2) p_hbm_gather(Args a, const uint32_t* 
 // MLP-k dependent random gathers: k independent chains per thread, one 4-B load
 // per 32-B sector, over `mask+1` sectors.  Tells whether random HBM reads are
 // latency-bound (rate grows with k) or transaction-bound (flat in k).
-template <int K>
+// OP: cache operator of the load -- 0 ld.global.nc (L1-allocating read-only),
+// 1 ld.global.nc.L1::no_allocate, 2 ld.global.cg (L2 only), 3 ld.global.ca (round 2).
+template <int OP>
+__device__ __forceinline__ uint32_t gather_load(const uint32_t* p) {
+    uint32_t w;
+    if constexpr (OP == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w) : "l"(p));
+    else if constexpr (OP == 1) asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(w) : "l"(p));
+    else if constexpr (OP == 2) asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(w) : "l"(p));
+    else asm volatile("ld.global.ca.b32 %0, [%1];" : "=r"(w) : "l"(p));
+    return w;
+}
+
+template <int K, int OP = 0>
 __global__ void __launch_bounds__(1024, 2) p_hbm_gather_mlp(Args a, const uint32_t* __restrict__ buf, uint32_t mask) {
     uint32_t x[K];
 #pragma unroll
@@ -112,8 +124,7 @@ __global__ void __launch_bounds__(1024, 2) p_hbm_gather_mlp(Args a, const uint32
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             x[k] = x[k] * 1664525u + 1013904223u;
-            uint32_t w;
-            asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w) : "l"(buf + ((x[k] >> 3) & mask) * 8u));
+            const uint32_t w = gather_load<OP>(buf + ((x[k] >> 3) & mask) * 8u);
             x[k] ^= w;
         }
     }
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(1024, 2) p_hbm_gather_mlp(Args a, const uint32
     if (s == 0x12345679u) a.sink[0] = s;
 }
 
-int gather_only(size_t mb) {
+int gather_only(size_t mb, int op) {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     Args a{};
@@ -141,7 +152,9 @@ int gather_only(size_t mb) {
     float best = 1e30f;
     for (int rep = 0; rep < 3; ++rep) {
         CK(cudaEventRecord(e0));
-        p_hbm_gather_mlp<1><<<2 * sms, 1024>>>(a, buf, mask);
+        void (*fns[])(Args, const uint32_t*, uint32_t) = {p_hbm_gather_mlp<1, 0>, p_hbm_gather_mlp<1, 1>,
+                                                          p_hbm_gather_mlp<1, 2>, p_hbm_gather_mlp<1, 3>};
+        fns[op & 3]<<<2 * sms, 1024>>>(a, buf, mask);
         CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1));
         float ms;
@@ -149,13 +162,14 @@ int gather_only(size_t mb) {
         if (ms < best) best = ms;
     }
     double picks = double(2 * sms) * 1024 * a.iters;
-    printf("{\"probe\": \"hbm_gather_mlp\", \"mib\": %zu, \"mlp\": 1, \"picks_per_s\": %.4e, \"ms\": %.3f}\n",
-           mb, picks / (best * 1e-3), best);
+    printf("{\"probe\": \"hbm_gather_mlp\", \"mib\": %zu, \"mlp\": 1, \"op\": %d, \"picks_per_s\": %.4e, \"ms\": %.3f}\n",
+           mb, op, picks / (best * 1e-3), best);
     return 0;
 }
 
 int main(int argc, char** argv) {
-    if (argc > 2 && strcmp(argv[1], "gather") == 0) return gather_only(strtoull(argv[2], nullptr, 10));
+    if (argc > 2 && strcmp(argv[1], "gather") == 0)
+        return gather_only(strtoull(argv[2], nullptr, 10), argc > 3 ? atoi(argv[3]) : 0);
     int dev = 0, sms = 0, clk = 0;
     CK(cudaSetDevice(dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -306,7 +306,7 @@ __device__ __forceinline__ void xorshift_split(uint32_t& lo, uint32_t& hi, const
 constexpr uint32_t kKR = 0x9E3779B1u, kKH = 0x85EBCA77u, kKX = 0xC2B2AE3Du;
 
 template <int P, bool SMEM, bool STRADDLE, int XS, int ADDR = 0, int LD = 0, int EXTRA = 0, bool COUNT = false,
-          int PROBE = 0, int MEMCOPY = 0>
+          int PROBE = 0, int MEMCOPY = 0, int BAL = 0>
 __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, uint32_t& xhi, uint32_t r,
                                            uint64_t base, uint32_t nc_mask, uint32_t src_lane,
                                            const KernelArgs& args, uint64_t policy = 0, bool inject = false,
@@ -402,6 +402,19 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
         static_assert(P == 1, "ADDR 8 is the P = 1 hybrid form");
+        if constexpr (LD == 1)        // round 2: global part without L1 allocation
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %1, %2;\n\t"
+                         "@p ld.shared.b32 %0, [%3];\n\t"
+                         "@!p ld.global.nc.L1::no_allocate.b32 %0, [%4];\n\t}"
+                         : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        else if constexpr (LD == 2)   // round 2: global part cached at L2 only
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %1, %2;\n\t"
+                         "@p ld.shared.b32 %0, [%3];\n\t"
+                         "@!p ld.global.cg.b32 %0, [%4];\n\t}"
+                         : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        else
         asm volatile("{\n\t.reg .pred p;\n\t"
                      "setp.lt.u32 p, %1, %2;\n\t"
                      "@p ld.shared.b32 %0, [%3];\n\t"
@@ -483,6 +496,12 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
     for (int j = 0; j < kAccum; ++j) {
         a[j] = a[j] * args.mul[j] + t;
         t = a[j] + rotl(t, rot_of(j));
+        // BAL > 0 (round-2 prototype of a pipe-balanced round, NOT SCS-2): BAL extra
+        // multiply-adds on the t chain, spread over R7 (t = t * odd + a[j ^ 8])
+        if constexpr (BAL > 0) {
+            if ((j + 1) % (kAccum / BAL) == 0 && (j + 1) / (kAccum / BAL) <= BAL)
+                t = t * args.mul[(j + 5) & 15] + a[j ^ 8];
+        }
     }
     // injected adversary work: dependent ALU ops that leave t unchanged (t ^ 0)
     if (inject) {
@@ -525,7 +544,7 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
 //            and logical grid, but all 32 warps of the SM progress together.
 template <int P, bool SMEM, bool STRADDLE, int XS, int UNROLL, int ADDR = 0, int LD = 0, int EXTRA = 0,
           bool COUNT = false, int EVERY = 0, int ILP = 1, int PROBE = 0, int PAD = 0, int SYNC = 0, int FEXTRA = 0,
-          int MEMCOPY = 0>
+          int MEMCOPY = 0, int BAL = 0>
 __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_checksum_kernel(const KernelArgs args) {
     __shared__ uint64_t red[32];
     __shared__ __align__(8) uint64_t bar;
@@ -654,7 +673,7 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
                     constexpr int kDep = (PROBE & 8) ? 8 : 0;
                     xlo[s] = a[(s + ILP - 1) % ILP][kDep] * args.zero + xlo[s];
                 }
-                scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE, MEMCOPY>(
+                scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE, MEMCOPY, BAL>(
                     a[s], xlo[s], xhi[s], r + u, base, nc_mask, src_lane, args, policy,
                     EVERY > 0 ? (u % EVERY == 0) : (u == 0), policy_lo);
 #pragma unroll
@@ -668,7 +687,7 @@ __global__ void __launch_bounds__(ILP <= 2 ? 1024 : 512, ILP == 1 ? 2 : 1) sage_
     for (; r < rounds; ++r) {
 #pragma unroll
         for (int s = 0; s < ILP; ++s)
-            scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE, MEMCOPY>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
+            scs_round<P, SMEM, STRADDLE, XS, ADDR, LD, EXTRA, COUNT, PROBE, MEMCOPY, BAL>(a[s], xlo[s], xhi[s], r, base, nc_mask, src_lane,
                                                                       args, policy, true, policy_lo);
     }
 

@@ -69,6 +69,15 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 #define VARE(U, PAD, EXTRA, EVERY) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD" #PAD " EXTRA" #EXTRA " EVERY" #EVERY, \
                   sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, EXTRA, false, EVERY, 2, 0, PAD>, 1, true, false, 2}
 
+// round 2: hybrid (ADDR 8) with the global part's cache operator LD (1 no L1 allocation, 2 .cg)
+#define VARH8L(U, ST, PAD, LD) {"P1 hybrid8 unroll" #U " ILP2 stage" #ST " PAD" #PAD " LD" #LD, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 8, LD, 0, false, 0, 2, 0, PAD>, 1, true, false, 2, 0, ST}
+// round 2: pipe-balanced round prototype (BAL extra multiply-adds per round; NOT SCS-2) +
+// EXTRA injected (the adversary) every round
+#define VARB(U, PAD, BAL, EXTRA) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD" #PAD " BAL" #BAL " EXTRA" #EXTRA, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, EXTRA, false, 1, 2, 0, PAD, 0, 0, 0, BAL>, \
+                  1, true, false, 2, 0, 0, 1}
+
 #define VARZ(XS, U, A, PAD) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD, \
                   sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
 
