@@ -8,9 +8,14 @@ register count, and -- with --run, on a B200 -- times every variant `--passes`
 times (3 launches each, best kept), checks they all return the same checksum,
 and prints the ranking.  The verifier's margin is the gap between the product
 and the fastest implementation anyone can build, so the
-search is kept runnable: an attacker can run it too.
+search is kept runnable: an attacker can run it too -- with --extra / --every it
+searches the schedule of the ADVERSARY's kernel (the c2a kernel with EXTRA
+result-neutral dependent instructions injected every EVERY rounds: EXTRA < 0
+IMADs on the FMA pipe, > 0 ALU ops), which is how the attacker-optimised margin
+of DESIGN.md section 11 was measured.
 
     python scripts/schedule_search.py --unroll 16-19 --pad 0-12 --out gpurun_out/search.jsonl --run
+    python scripts/schedule_search.py --unroll 8-36 --pad 0-12 --extra -1 --every 1 --run
 """
 import argparse
 import json
@@ -41,11 +46,25 @@ def grid(unrolls, pads, xss, addrs):
     return [(xs, u, a, p) for xs in xss for u in unrolls for a in addrs for p in pads]
 
 
-def build(points, binary):
-    """Compile bench/variants.cu with the generated list; return {point: registers}."""
+def variant_name(pt, extra=0, every=0):
+    xs, u, a, p = pt
+    if extra:
+        return "P1 smem xs16 unroll%d addr4 ILP2 PAD%d EXTRA%d EVERY%d" % (u, p, extra, every)
+    return "P1 smem xs%d unroll%d addr%d ILP2 PAD%d" % pt
+
+
+def build(points, binary, extra=0, every=0, reference=True):
+    """Compile bench/variants.cu with the generated list; return {point: registers}.
+    With extra != 0 the variants are the adversary's (VARE: XS 16, ADDR 4), and the
+    product kernel (VARZ 16/18/4/7) is compiled first as the reference."""
     with tempfile.NamedTemporaryFile("w", suffix=".inc", delete=False) as f:
+        if extra and reference:
+            f.write("    VARZ(16, 18, 4, 7),\n")
         for xs, u, a, p in points:
-            f.write("    VARZ(%d, %d, %d, %d),\n" % (xs, u, a, p))
+            if extra:
+                f.write("    VARE(%d, %d, %d, %d),\n" % (u, p, extra, every))
+            else:
+                f.write("    VARZ(%d, %d, %d, %d),\n" % (xs, u, a, p))
         inc = f.name
     try:
         subprocess.check_call(["nvcc"] + ARCH + ["-O3", "-lineinfo", "-std=c++17",
@@ -62,10 +81,12 @@ def build(points, binary):
             name = m.group(1)
         m = re.search(r"REG:(\d+)", ln)
         if m and name:
-            t = re.search(r"kernelILi1ELb1ELb0ELi(\d+)ELi(\d+)ELi(\d+)ELi0ELi0ELb0ELi0ELi2ELi0ELi(\d+)E", name)
+            t = re.search(r"kernelILi1ELb1ELb0ELi(\d+)ELi(\d+)ELi(\d+)ELi0ELin?(\d+)ELb0ELi(\d+)ELi2ELi0ELi(\d+)E",
+                          name)
             if t:
-                xs, u, a, p = (int(v) for v in t.groups())
-                regs[(xs, u, a, p)] = int(m.group(1))
+                xs, u, a, ex, ev, p = (int(v) for v in t.groups())
+                if (ex != 0) == bool(extra):
+                    regs[(xs, u, a, p)] = int(m.group(1))
     return regs
 
 
@@ -98,9 +119,12 @@ def main():
     ap.add_argument("--binary", default=os.path.join(ROOT, "bench", "variants_search"))
     ap.add_argument("--out", default=None)
     ap.add_argument("--run", action="store_true", help="time the variants (needs a B200)")
+    ap.add_argument("--extra", type=int, default=0, help="adversary: injected instructions (<0 IMAD, >0 ALU)")
+    ap.add_argument("--every", type=int, default=1, help="adversary: inject every EVERY rounds")
+    ap.add_argument("--no-build", action="store_true", help="time an already built --binary")
     a = ap.parse_args()
     points = grid(parse_range(a.unroll), parse_range(a.pad), parse_range(a.xs), parse_range(a.addr))
-    regs = build(points, a.binary)
+    regs = {} if a.no_build else build(points, a.binary, a.extra, a.every)
     print(json.dumps({"built": len(points), "binary": a.binary}), flush=True)
     if not a.run:
         for pt in points:
@@ -108,13 +132,18 @@ def main():
         return 0
     times, same = run(a.binary, a.passes, a.rounds, a.bytes)
     rows = []
+    ref = times.get(variant_name((16, 18, 4, 7))) if a.extra else None
     for pt in points:
-        name = "P1 smem xs%d unroll%d addr%d ILP2 PAD%d" % pt
+        name = variant_name(pt, a.extra, a.every)
         if name in times:
             r = regs.get(pt)
-            rows.append({"xs": pt[0], "unroll": pt[1], "addr": pt[2], "pad": pt[3], "registers": r,
-                         "full_register_file": r is not None and 56 < r <= 64, "ms": min(times[name]),
-                         "ms_all": times[name]})
+            row = {"xs": pt[0], "unroll": pt[1], "addr": pt[2], "pad": pt[3], "registers": r,
+                   "full_register_file": r is not None and 56 < r <= 64, "ms": min(times[name]),
+                   "ms_all": times[name]}
+            if a.extra:
+                row.update(extra=a.extra, every=a.every, product_ms=min(ref) if ref else None,
+                           slowdown_vs_product=(min(times[name]) / min(ref) - 1.0) if ref else None)
+            rows.append(row)
     rows.sort(key=lambda d: d["ms"])
     lines = [json.dumps(dict(d, same_checksum=same)) for d in rows]
     if a.out:
