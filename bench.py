@@ -21,15 +21,17 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from bench.clocks import ClockSampler  # noqa: E402
+
 METRIC = "checksum rounds/s and checksummed GB/s per B200 (1/2/4/8 GPU); p99 attest time"
 UNIT = "thread-rounds/s"
 ATTEST_SAMPLES, ATTEST_BUDGET_S = 200, 15.0   # attest_ms distribution: up to 200 runs / ~15 s
+EXTRA_CONFIGS, EXTRA_STEPS = ("c2c", "c3p1", "c3p8"), 5   # timed beside c2a in the same run ("extra")
 CPU_SAMPLE_S = 20.0          # cpu_baseline sizing target (the one-warp-per-core calibration pass
                              # overestimates the per-warp cost ~2x, so the timed sample runs ~10 s)
 
@@ -61,9 +63,9 @@ def load_peaks():
 
 
 def load_traffic(workload, thread_rounds):
-    """DRAM bytes (read + write) per launch from the committed ncu --set full
-    summary (profiles/ncu_traffic.json), or None.  Entries give bytes per
-    launch, or bytes per thread-round (scaled to this launch's n*R)."""
+    """DRAM bytes (read + write) per launch from the committed ncu summary
+    (profiles/ncu_traffic.json), or None.  Entries give bytes per launch, or bytes
+    per thread-round (scaled to this launch's n*R)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
@@ -91,59 +93,33 @@ def random_gather_ceiling(region_bytes):
         return None
 
 
-class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
-
-    def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm, smax, reasons, power = [], None, set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-                power.append(float(parts[3]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[5:9]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        busy = [v for v in sm if smax and v > 0.5 * smax] or sm
-        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm),
-                "power_w_median": statistics.median(power) if power else None}
+def roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, workload, gather_ceiling=None):
+    """Roofline record of the checksum kernel.  HBM regions
+    (GLOBAL, > 1 MiB): one 32-B DRAM sector per pick against hbm_gbs; everything
+    else: algorithmic 32-bit integer ops per thread-round against the issue peak."""
+    f_clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    traffic = load_traffic(workload, n * R)
+    if placement == "global" and nbytes > (1 << 20):
+        achieved = n * R * 32.0 / mean_k / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "peak_source": peak_src + " hbm_gbs (copy)",
+                "achieved_def": "one 32-B sector per pick x n x R / kernel time",
+                "random_gather_ceiling_picks_per_s": gather_ceiling,
+                "frac_of_random_gather_ceiling": (n * R / mean_k / gather_ceiling) if gather_ceiling else None}
+    ops = OPS_PER_ROUND[P]
+    peak_ops = sms * 4 * 32 * f_clk / 1e12
+    achieved = n * R * ops / mean_k / 1e12
+    rf = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s", "frac": achieved / peak_ops,
+          "traffic": traffic, "ops_per_thread_round": ops,
+          "peak_source": "%d SMs x 4 SMSP x 32 lanes x 1 issue/clk x %s sm_max_mhz %.0f (DESIGN.md 7)"
+                         % (sms, peak_src, f_clk / 1e6)}
+    if placement == "hybrid":
+        rf["binding_limit"] = ("L1->L2 miss requests, not the ALU: 62.5% of the picks miss the 192 KiB staged "
+                               "prefix (DESIGN.md section 7); frac is the integer-issue fraction")
+    elif placement == "global":
+        rf["binding_limit"] = "L1/L2 pick latency and requests (L2-resident region), DESIGN.md section 7"
+    return rf
 
 
 def dist_env():
@@ -163,17 +139,29 @@ def cpu_oracle_rate(pool, nonce, base, rounds, warps, P):
     return len(warps) * 32 * rounds / dt, dt, sums
 
 
+def reference_region(nbytes, P):
+    """The workload's region for the oracle arm: the launched kernel's code + PCG64
+    fill when a GPU is there to ask which kernel that is (content does not change
+    the oracle's speed), else the fill alone."""
+    from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region
+    prefix = b""
+    try:
+        import torch
+        if torch.cuda.is_available() and nbytes <= (1 << 20):
+            prefix = launched_kernel_prefix(nbytes, pick_words=P)
+    except Exception:                                # no GPU / library: timing is content-independent
+        prefix = b""
+    return make_region(nbytes, prefix=prefix)
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import numpy as np  # noqa: F401
     import oracle
-    from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region
     nbytes, P, R, desc = CONFIGS[args.config]
     oracle.build()
-    region = make_region(nbytes, prefix=kernel_code_prefix(P, nbytes <= 65536)) if nbytes <= (1 << 20) else \
-        make_region(nbytes)
+    region = reference_region(nbytes, P)
     cores = len(os.sched_getaffinity(0))
     base = 0x7F00_0000_0000
     sample_warps = list(range(4 * cores))
@@ -199,12 +187,114 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- our arm
+def make_device_region(ctx, nbytes, dev):
+    """The workload's region on the device: the machine code of the kernel this
+    context launches for it (self-verification) followed by a
+    seeded pseudo-random fill (PCG64 on the host up to 1 MiB; a seeded torch
+    generator on the device for HBM-sized regions).  Returns (device tensor,
+    host copy or None)."""
+    import torch
+    from paper_2209_03125_b200.inputs import REGION_FILL_SEED, kernel_code_prefix, make_region
+    code = kernel_code_prefix(ctx, nbytes)
+    if nbytes <= (1 << 20):
+        region_np = make_region(nbytes, prefix=code)
+        return torch.from_numpy(region_np).to(dev), region_np
+    g = torch.Generator(device=dev)
+    g.manual_seed(REGION_FILL_SEED)
+    region = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
+    if code:
+        region[:len(code)].copy_(torch.frombuffer(bytearray(code), dtype=torch.uint8))
+    return region, None
+
+
+def warm_up(ctx, region, R, nonces, warmup, steps, stream, dev, flush):
+    """Allocate the raw results and per-step CUDA events (on the launching stream)
+    for warmup + steps attestations and run the warmup ones, each preceded by an L2
+    flush (a 256 MiB fill).  Returns (raw, events, launch count after warmup)."""
+    import torch
+    from paper_2209_03125_b200 import sage
+    total = warmup + steps
+    raw = torch.zeros(total, 4, dtype=torch.int64, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(total)]
+    for k in range(warmup):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        ctx.attest_async(nonces[k], region, R, raw[k])
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launches
+    return raw, ev, launches0
+
+
+def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms, args):
+    """Secondary BASELINE configs timed in the same process (the driver's record of
+    them): c2c (the paper's 524,288-B buffer, SAGE_HYBRID), c3p1 / c3p8 (256 MiB in
+    HBM), each with kernel time, roofline fraction, DRAM traffic and clocks; plus
+    the attestation wall-time distribution at R = 10^4 (config 4's shortest)."""
+    import torch
+    from paper_2209_03125_b200 import replicas, sage, verifier
+    out = {}
+    nonces = replicas.replica_nonces(17, 64)
+    for name in EXTRA_CONFIGS:
+        nbytes, P, R, desc = CONFIGS[name]
+        ctx = sage.Context(pick_words=P, stream=stream, **ctx_args)
+        region, _ = make_device_region(ctx, nbytes, dev)
+        info = ctx.query()
+        n = info.blocks * info.threads
+        placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
+        ceiling = random_gather_ceiling(nbytes) if nbytes > (1 << 20) else None
+        raw, ev, _ = warm_up(ctx, region, R, nonces, 2, 0, stream, dev, flush)
+        sampler = ClockSampler(dev.index).start()
+        launches0 = ctx.launches
+        kern = []
+        for k in range(EXTRA_STEPS):
+            flush.fill_(k & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.attest_async(nonces[2 + k], region, R, raw[0])
+            e1.record(stream)
+            kern.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        clocks = sampler.stop()
+        ks = [a.elapsed_time(b) / 1e3 for a, b in kern]
+        mean_k = statistics.mean(ks)
+        out[name] = {"desc": desc, "region_bytes": nbytes, "P": P, "rounds": R, "placement": placement,
+                     "steps": EXTRA_STEPS, "gpu_launches": ctx.launches - launches0,
+                     "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(ks), "max": 1e3 * max(ks)},
+                     "thread_rounds_per_s": n * R / mean_k, "checksummed_gbps": n * R * 4 * P / mean_k / 1e9,
+                     "roofline": roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, name, ceiling),
+                     "clocks": clocks}
+        ctx.close()
+        del region
+    # config 4's shortest round count: the verifier's wall time, c2a geometry
+    nbytes, P, _, _ = CONFIGS["c2a"]
+    ctx = sage.Context(stream=stream, **ctx_args)
+    region, _ = make_device_region(ctx, nbytes, dev)
+    for k in range(3):
+        ctx.attest(nonces[k], region, 10_000)
+    att = []
+    t0 = time.perf_counter()
+    for k in range(ATTEST_SAMPLES):
+        att.append(ctx.attest(nonces[k % 64], region, 10_000).elapsed_ns / 1e6)
+        if time.perf_counter() - t0 > ATTEST_BUDGET_S:
+            break
+    out["attest_ms_r1e4"] = attest_stats(att, verifier)
+    ctx.close()
+    return out
+
+
+def attest_stats(att, verifier):
+    return {"p50": statistics.median(att), "p99": _pct(att, 99), "mean": statistics.mean(att),
+            "sigma": statistics.pstdev(att), "threshold_2p5sigma": statistics.mean(att) + 2.5 * statistics.pstdev(att),
+            "threshold_robust": (verifier.calibrate_robust(att, min_runs=1).threshold if len(att) >= 3 else None),
+            "n": len(att)}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2209_03125_b200 import build, replicas, sage, verifier
-    from paper_2209_03125_b200.inputs import kernel_code_prefix, make_region
 
     ws, rank, local = dist_env()
     if not torch.cuda.is_available():
@@ -230,38 +320,21 @@ def run_ours(args):
     nbytes, P, R, desc = CONFIGS[args.config]
     if args.rounds:
         R = args.rounds
-    smem = nbytes <= 65536
-    if nbytes <= (1 << 20):
-        region_np = make_region(nbytes, prefix=kernel_code_prefix(P, smem))
-        region = torch.from_numpy(region_np).to(dev)
-    else:
-        region_np = None
-        g = torch.Generator(device=dev)
-        g.manual_seed(0x5EED0001)
-        region = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev, generator=g)
-    gather_ceiling = random_gather_ceiling(nbytes) if (rank == 0 and nbytes > (1 << 20)) else None
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     blocks, threads = (1, 32) if args.config == "c1" else (0, 0)
     ctx = sage.Context(device=local, blocks=blocks, threads=threads, pick_words=P, stream=stream)
+    region, region_np = make_device_region(ctx, nbytes, dev)
+    gather_ceiling = random_gather_ceiling(nbytes) if (rank == 0 and nbytes > (1 << 20)) else None
     info = ctx.query()
     n = info.blocks * info.threads
     placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
     my_nonces = replicas.replica_nonces(rank, args.warmup + args.steps + 64)
     total = args.warmup + args.steps
-    raw = torch.zeros(total, 4, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(total)]
+    raw, ev, _ = warm_up(ctx, region, R, my_nonces, args.warmup, args.steps, stream, dev, flush)
 
-    for k in range(args.warmup):
-        flush.fill_(k & 0xFF)
-        ev[k][0].record(stream)
-        ctx.attest_async(my_nonces[k], region, R, raw[k])
-        ev[k][1].record(stream)
-    torch.cuda.synchronize(dev)
-
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler = ClockSampler(local).start()                  # every rank samples its own GPU
     launches0 = ctx.launches
     if ws > 1:
         dist.barrier()
@@ -288,25 +361,21 @@ def run_ours(args):
     # e2e through the public C API with HOST buffers (pinned): H2D of the
     # region + kernel + D2H of the 32-byte result, every step.
     host_region = (torch.from_numpy(region_np) if region_np is not None else region.cpu()).pin_memory()
-    e2e = None
-    if host_region is not None:
-        ctx_h = sage.Context(device=local, blocks=blocks, threads=threads, pick_words=P, stream=stream)
-        for k in range(min(2, args.warmup)):
-            ctx_h.attest_host(my_nonces[k], host_region, R)
-        torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        e2e_ns = []
-        for k in range(args.steps):
-            r = ctx_h.attest_host(my_nonces[args.warmup + k], host_region, R)
-            e2e_ns.append(r.elapsed_ns)
-        t_e2e = replicas.max_over_ranks(time.perf_counter() - t0, pdev)
-        e2e = {"value": ws * n * R * args.steps / t_e2e, "unit": UNIT,
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32,
-               "api": "sage_attest_host (pinned host region)",
-               "l2": "not flushed: each step's H2D copy rewrites the region just before the kernel reads it"}
-        ctx_h.close()
+    ctx_h = sage.Context(device=local, blocks=blocks, threads=threads, pick_words=P, stream=stream)
+    for k in range(min(2, args.warmup)):
+        ctx_h.attest_host(my_nonces[k], host_region, R)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        ctx_h.attest_host(my_nonces[args.warmup + k], host_region, R)
+    t_e2e = replicas.max_over_ranks(time.perf_counter() - t0, pdev)
+    e2e = {"value": ws * n * R * args.steps / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32,
+           "api": "sage_attest_host (pinned host region)",
+           "l2": "not flushed: each step's H2D copy rewrites the region just before the kernel reads it"}
+    ctx_h.close()
 
     # attestation wall time as the verifier sees it (sage_attest, device region):
     # ATTEST_SAMPLES attestations (at least --steps) or ATTEST_BUDGET_S of them,
@@ -324,10 +393,12 @@ def run_ours(args):
     dbg = ctx.attest_debug(0x1234, region, R, pw)
     parts = [int(v) & (2**64 - 1) for v in pw.cpu().tolist()]
 
-    # gather per-replica results to rank 0 (the only cross-GPU step, 8(e))
+    # gather per-replica records to rank 0 (the only cross-GPU step, 8(e)): every
+    # rank's own clocks, power and throttle reasons, kernel times and checksum
     mine = {"rank": rank, "device": local, "nonce": "0x%016x" % my_nonces[total - 1],
             "checksum": "0x%016x" % dec[-1].checksum, "cycles": dec[-1].cycles,
             "device_ns": dec[-1].device_ns, "kernel_ms_mean": 1e3 * statistics.mean(kern_s),
+            "kernel_ms_max": 1e3 * max(kern_s), "wall_s": t_wall, "clocks": clocks,
             "sampled_parity_sum_ok": (sum(parts) & (2**64 - 1)) == dbg.checksum}
     allr = replicas.gather_results(mine)
 
@@ -335,8 +406,6 @@ def run_ours(args):
         peaks, peak_src = load_peaks()
         mean_k = statistics.mean(kern_s)
         value = ws * n * R * args.steps / t_bracket
-        ops = OPS_PER_ROUND[P]
-        f_clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
         sms = info.sm_count
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * t_bracket / args.steps, "higher_is_better": True,
@@ -345,36 +414,18 @@ def run_ours(args):
                            "blocks": info.blocks, "threads": info.threads, "threads_total": n,
                            "placement": placement, "lane_states_per_thread": dbg.ilp,
                            "hw_grid": "%d x %d" % (info.blocks // dbg.ilp, info.threads),
+                           "kernel": ctx.kernel_symbol(nbytes, region.data_ptr()),
                            "parallelism": "independent replica per GPU x%d" % ws,
                            "plumbing": backend or "none",
                            "l2": "256 MiB buffer written between timed steps (flush)"},
                 "checksummed_gbps": value * 4 * P / 1e9,
                 "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(kern_s), "max": 1e3 * max(kern_s)},
-                "attest_ms": {"p50": statistics.median(att), "p99": _pct(att, 99), "mean": statistics.mean(att),
-                              "sigma": statistics.pstdev(att), "threshold_2p5sigma":
-                              statistics.mean(att) + 2.5 * statistics.pstdev(att),
-                              "threshold_robust": (verifier.calibrate_robust(att, min_runs=1).threshold
-                                                   if len(att) >= 3 else None), "n": len(att)},
+                "attest_ms": attest_stats(att, verifier),
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
         if clocks.get("power_w_median"):
             line["energy_j_per_attestation"] = clocks["power_w_median"] * mean_k
-        if placement == "global" and nbytes > (1 << 20):
-            achieved = n * R * 32.0 / mean_k / 1e9       # DRAM sectors touched (one 32-B sector per pick)
-            ceil = gather_ceiling
-            line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic(args.config, n * R),
-                                "peak_source": peak_src + " hbm_gbs (copy)",
-                                "achieved_def": "one 32-B sector per pick x n x R / kernel time",
-                                "random_gather_ceiling_picks_per_s": ceil,
-                                "frac_of_random_gather_ceiling": (n * R / mean_k / ceil) if ceil else None}
-        else:
-            peak_ops = sms * 4 * 32 * f_clk / 1e12
-            achieved = n * R * ops / mean_k / 1e12
-            line["roofline"] = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
-                                "frac": achieved / peak_ops, "traffic": load_traffic(args.config, n * R),
-                                "peak_source": "%d SMs x 4 SMSP x 32 lanes x 1 issue/clk x %s sm_max_mhz %.0f "
-                                               "(DESIGN.md 7)" % (sms, peak_src, f_clk / 1e6),
-                                "ops_per_thread_round": ops}
+        line["roofline"] = roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, args.config,
+                                    gather_ceiling)
         if ws > 1:
             line["replicas"] = allr
         if ws == 1 and not args.no_cpu_baseline:
@@ -401,6 +452,10 @@ def run_ours(args):
                                     "single_core_value": rate1,
                                     "single_core_sample": "%d warps (%.1f s)" % (len(sample[:4]), dt1),
                                     "parity_on_sample": ok}
+        if ws == 1 and not args.no_extra and args.config == "c2a":
+            del flush
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+            line["extra"] = run_extra({"device": local}, dev, stream, flush, peaks, peak_src, sms, args)
         print(json.dumps(line), flush=True)
     ctx.close()
     if ws > 1:
@@ -426,6 +481,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=0, help="override the workload's round count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs (c2c, c3p1, c3p8, R=1e4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -36,13 +36,15 @@ def max_over_ranks(value, device=None):
     return float(t.item())
 
 
-def gather_results(record):
-    """All replicas' result records (dicts), in rank order, on every rank."""
-    ws, _ = world()
+def gather_results(record, dst=0):
+    """Every replica's result record (dicts), in rank order, on rank `dst` (None on
+    the other ranks): the only cross-GPU exchange of the path, after all kernels
+    finished (torch.distributed.gather_object)."""
+    ws, rank = world()
     if ws == 1:
         return [record]
-    out = [None] * ws
-    dist.all_gather_object(out, record)
+    out = [None] * ws if rank == dst else None
+    dist.gather_object(record, out, dst=dst)
     return out
 
 

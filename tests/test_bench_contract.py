@@ -58,6 +58,17 @@ def test_our_arm_one_gpu():
     assert cb["kind"] == "oracle" and cb["parity_on_sample"] is True and cb["cores"] >= 1
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
     assert line["attest_ms"]["p99"] >= line["attest_ms"]["p50"] > 0
+    assert line["config"]["kernel"].startswith("_ZN4sage20sage_checksum_kernel")
+    # the secondary configs timed in the same process
+    ex = line["extra"]
+    assert set(ex) == {"c2c", "c3p1", "c3p8", "attest_ms_r1e4"}
+    for name in ("c2c", "c3p1", "c3p8"):
+        e = ex[name]
+        assert e["steps"] == 5 and e["gpu_launches"] == 5 and e["kernel_ms"]["mean"] > 0
+        assert 0 < e["roofline"]["frac"] <= 1 and {"sm_mhz", "reasons"} <= set(e["clocks"])
+    assert ex["c2c"]["placement"] == "hybrid" and "binding_limit" in ex["c2c"]["roofline"]
+    assert ex["c3p1"]["roofline"]["bound"] == "hbm" and ex["c3p8"]["roofline"]["bound"] == "hbm"
+    assert ex["attest_ms_r1e4"]["p50"] > 0
 
 
 @pytest.mark.gpu
@@ -68,4 +79,6 @@ def test_our_arm_two_replicas_torchrun():
     assert len(reps) == 2 and {r["rank"] for r in reps} == {0, 1}
     assert reps[0]["nonce"] != reps[1]["nonce"]       # an independent nonce stream per replica
     assert all(r["sampled_parity_sum_ok"] for r in reps)
+    assert all({"sm_mhz", "sm_max_mhz", "reasons", "power_w_median"} <= set(r["clocks"]) for r in reps)
+    assert all(r["kernel_ms_mean"] > 0 for r in reps)
     assert "cpu_baseline" not in line                 # rank 0 at N=1 only

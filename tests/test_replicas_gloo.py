@@ -1,6 +1,7 @@
 """Multi-process (world_size 2, gloo, CPU) test of the replica plumbing:
-independent nonces per rank, result gather to rank 0, max-over-ranks timing,
-and the rank-0 verification of every replica.  The per-rank checksum comes
+independent nonces per rank, result gather to rank 0 only (each record carrying
+that rank's own clock sampler summary), max-over-ranks timing, and the rank-0
+verification of every replica.  The per-rank checksum comes
 from the oracle here (no GPU); on the box it comes from libsage.so."""
 import os
 import socket
@@ -22,6 +23,7 @@ def _worker(rank, ws, port, outq):
     import torch.distributed as dist
 
     import oracle
+    from bench.clocks import ClockSampler
     from paper_2209_03125_b200 import replicas
     from paper_2209_03125_b200.inputs import make_region
 
@@ -33,7 +35,10 @@ def _worker(rank, ws, port, outq):
         region = make_region(1024)
         base = 0x7F00_0000_0000 + rank * 0x1000
         cs = oracle.attest(nonce, region, base, 50, 1, 32)
-        rec = {"rank": rank, "nonce": nonce, "checksum": "0x%016x" % cs, "device_ns": 1000 + 500 * rank}
+        sampler = ClockSampler(rank).start()           # each rank samples its own GPU
+        clocks = sampler.stop()
+        rec = {"rank": rank, "nonce": nonce, "checksum": "0x%016x" % cs, "device_ns": 1000 + 500 * rank,
+               "clocks": clocks}
         allr = replicas.gather_results(rec)
         tmax = replicas.max_over_ranks(1.0 + rank)
         if rank == 0:
@@ -43,6 +48,7 @@ def _worker(rank, ws, port, outq):
             outq.put({"records": allr, "tmax": tmax, "ok": ok})
         else:
             assert tmax == 2.0
+            assert allr is None                          # gathered to rank 0 only
         assert np.isfinite(tmax)
     finally:
         dist.destroy_process_group()
@@ -65,6 +71,9 @@ def test_two_replicas_gather_and_verify():
     assert res["records"][0]["checksum"] != res["records"][1]["checksum"]
     assert res["tmax"] == 2.0
     assert res["ok"] == {0: True, 1: True}
+    # every replica's record carries its own GPU's clock record
+    assert [r["clocks"]["gpu"] for r in res["records"]] == [0, 1]
+    assert all({"sm_mhz", "sm_max_mhz", "reasons", "samples"} <= set(r["clocks"]) for r in res["records"])
 
 
 def test_single_process_fallbacks():
