@@ -33,19 +33,25 @@ struct Adv {
 
 // <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA, COUNT, EVERY, ILP, PROBE, PAD, SYNC, FEXTRA, MEMCOPY>
 // The product's c2a kernel is <1, SMEM, nostraddle, XS 16, UNROLL 18, ADDR 4, ILP 2, PAD 7>.
+// The attacker's schedules: the fastest points of scripts/schedule_search.py run over
+// the adversary's own kernel (UNROLL 8-36 x PAD 0-12 for +1 IMAD / round, 377 points;
+// UNROLL 7..35 step 7 x PAD 0-12 for +1 IMAD / 7 rounds, 65 points; profiles/r02/):
+// UNROLL 9 / PAD 1 (+0.054% vs the product) and UNROLL 7 / PAD 10 (+1.27%).
 #ifndef ADV_ATK_U
-#define ADV_ATK_U 17        // attacker-searched schedule for +1 IMAD / round (profiles/r02/attacker_search*.jsonl)
-#define ADV_ATK_PAD 7
+#define ADV_ATK_U 9
+#define ADV_ATK_PAD 1
 #endif
 #ifndef ADV_ATK7_U
-#define ADV_ATK7_U 14       // attacker-searched schedule for +1 IMAD / 7 rounds
-#define ADV_ATK7_PAD 7
+#define ADV_ATK7_U 7
+#define ADV_ATK7_PAD 10
 #endif
 const Adv kAdv[] = {
     {"+1 IMAD / round (product schedule)",
      sage_lab::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, -1, false, 1, 2, 0, 7>, 2, 0},
     {"+1 ALU op / 18 rounds (product schedule)",
      sage_lab::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 1, false, 18, 2, 0, 7>, 2, 0},
+    {"+1 IMAD / round (attacker-searched schedule, 2nd best: UNROLL 17 / PAD 7)",
+     sage_lab::sage_checksum_kernel<1, true, false, 16, 17, 4, 0, -1, false, 1, 2, 0, 7>, 2, 0},
     {"+1 IMAD / round (attacker-searched schedule)",
      sage_lab::sage_checksum_kernel<1, true, false, 16, ADV_ATK_U, 4, 0, -1, false, 1, 2, 0, ADV_ATK_PAD>, 2, 0},
     {"+1 IMAD / 7 rounds (attacker-searched schedule)",

@@ -5,7 +5,8 @@ back within the expected time.  The time threshold is
 T_avg + 2.5 sigma over calibration runs (Table 1 row
 "T_avg + 2.5 sigma"); calibrate_quantile and
 calibrate_robust (median/MAD, for B200's non-normal run times) are the
-alternatives measured in DESIGN.md section 11.  Rejection is a verdict, not an
+alternatives measured in DESIGN.md section 11; calibrate_session / verify_session
+bound the median of a session's series of challenges.  Rejection is a verdict, not an
 error; on a rejection the session restarts with a fresh challenge.
 
 This is plain host arithmetic over measured numbers; the checksum itself is
@@ -32,7 +33,7 @@ class TimingModel:
 @dataclass(frozen=True)
 class Verdict:
     accepted: bool
-    reason: str               # ok | checksum_mismatch | timeout | stale_nonce
+    reason: str               # ok | checksum_mismatch | timeout | stale_nonce | session_timeout
     elapsed: float
     expected: int
     response: int
@@ -119,6 +120,62 @@ class RobustTimingModel:
     @property
     def threshold(self):
         return self.median * (1.0 + self.margin)
+
+
+def calibrate_session(samples, m, k=6.0, min_margin=2e-4, min_runs=30):
+    """Timing model for a SESSION of m attestations: the paper's verifier "invokes
+    [the VF] repeatedly with a series of challenges while measuring the VF execution
+    time for each invocation", so besides each run's own deadline it can
+    test the session's median run time.  The median of m runs has standard error
+    ~1.2533 * sigma / sqrt(m) (sigma: the main mode's scale, sigma_r = 1.4826 * MAD of
+    the honest calibration runs), so threshold = median * (1 + margin) with margin =
+    max(min_margin, k * 1.2533 * sigma_r / (sqrt(m) * median)).  A run hit by one of
+    B200's ~1.7 ms whole-chip pauses moves the session median by one rank only.
+    This is what separates an attacker whose own schedule search hides one extra
+    IMAD per round within a single run's noise (+0.05-0.08% at R = 10^5, DESIGN.md
+    section 11) from honest sessions; the 0.02% floor is ~7x the main mode's drift
+    over a config-4 capture (0.003%)."""
+    xs = [float(s) for s in samples]
+    if len(xs) < min_runs:
+        raise ValueError("calibration needs >= %d runs, got %d" % (min_runs, len(xs)))
+    if m < 1 or k <= 0 or min_margin < 0:
+        raise ValueError("need m >= 1, k > 0 and min_margin >= 0")
+    med = percentile(xs, 50.0)
+    sigma_r = 1.4826 * percentile([abs(x - med) for x in xs], 50.0)
+    margin = max(min_margin, k * 1.2533 * sigma_r / (math.sqrt(m) * med))
+    return SessionTimingModel(median=med, sigma_r=sigma_r, m=m, runs=len(xs), margin=margin)
+
+
+@dataclass(frozen=True)
+class SessionTimingModel:
+    median: float
+    sigma_r: float
+    m: int
+    runs: int
+    margin: float
+
+    @property
+    def threshold(self):
+        """Bound on the median run time of a session of m attestations."""
+        return self.median * (1.0 + self.margin)
+
+
+def verify_session(results, model, ledger=None):
+    """Verdict on a session of model.m attestations, results = [(nonce, response,
+    elapsed, expected), ...]: rejected with the first failing run's reason if any
+    checksum is wrong or a nonce is reused; otherwise rejected as "session_timeout"
+    iff the median elapsed time exceeds model.threshold.  Returns a Verdict whose
+    elapsed field is the session median."""
+    if len(results) != model.m:
+        raise ValueError("a session has %d attestations, got %d" % (model.m, len(results)))
+    for nonce, response, elapsed, expected in results:
+        if ledger is not None and not ledger.consume(nonce):
+            return Verdict(False, "stale_nonce", elapsed, expected, response)
+        if response != expected:
+            return Verdict(False, "checksum_mismatch", elapsed, expected, response)
+    med = percentile([r[2] for r in results], 50.0)
+    ok = med <= model.threshold
+    return Verdict(ok, "ok" if ok else "session_timeout", med, results[-1][3], results[-1][1])
 
 
 def stall_estimate(samples, floor=1e-3):

@@ -2,6 +2,8 @@
 import math
 import random
 
+import numpy as np
+
 import pytest
 
 from paper_2209_03125_b200 import verifier as V
@@ -164,3 +166,49 @@ def test_stall_estimate_recovers_injected_pauses():
     assert est["excess_median_s"] == pytest.approx(0.0017)
     assert est["rate_per_s"] == pytest.approx(-math.log(1 - 0.025) / T)
     assert V.stall_estimate([T] * 10)["rate_per_s"] == 0.0
+
+
+def test_session_model_closed_form_and_checks():
+    """calibrate_session: margin = max(floor, k * 1.2533 * sigma_r / (sqrt(m) * median)),
+    sigma_r = 1.4826 * MAD; verify_session rejects a wrong checksum or a reused nonce
+    before looking at time, and thresholds the session median."""
+    xs = [100.0 + d for d in (-2, -1, 0, 1, 2)] * 6          # median 100, MAD 1
+    m = V.calibrate_session(xs, m=16, k=6.0, min_margin=0.0)
+    assert m.median == 100.0 and m.sigma_r == pytest.approx(1.4826)
+    assert m.margin == pytest.approx(6 * 1.2533 * 1.4826 / (4 * 100.0))
+    assert V.calibrate_session(xs, m=16, min_margin=0.5).margin == 0.5
+    runs = [(n, 7, 100.0, 7) for n in range(16)]
+    assert V.verify_session(runs, m).accepted
+    slow = [(n, 7, 103.0, 7) for n in range(16)]
+    assert V.verify_session(slow, m).reason == "session_timeout"
+    bad = runs[:5] + [(99, 8, 100.0, 7)] + runs[6:]
+    assert V.verify_session(bad, m).reason == "checksum_mismatch"
+    led = V.NonceLedger()
+    led.consume(3)
+    assert V.verify_session(runs, m, ledger=led).reason == "stale_nonce"
+    with pytest.raises(ValueError):
+        V.verify_session(runs[:15], m)
+
+
+def test_session_median_separates_a_small_shift_that_single_runs_cannot():
+    """Synthetic B200-like run times (main mode sigma 0.02%, 1% of runs paused by
+    +3%): an adversary +0.07% slower passes the single-run robust rule most of the
+    time, but every one of its 16-run sessions is rejected while honest sessions are
+    accepted, paused runs included."""
+    rng = np.random.default_rng(5)
+    T, s = 0.0538, 0.0002 * 0.0538
+
+    def runs(n, shift):
+        t = T * (1 + shift) + rng.normal(0, s, n)
+        t[rng.random(n) < 0.01] += 0.03 * T
+        return t
+
+    cal = runs(100, 0.0)
+    single = V.calibrate_robust(cal)
+    adv = runs(160, 0.0007)
+    assert np.mean(adv > single.threshold) < 0.5
+    sess = V.calibrate_session(cal, m=16)
+    sessions = lambda t: [V.verify_session([(i, 1, x, 1) for i, x in enumerate(t[j:j + 16])], sess).accepted
+                          for j in range(0, len(t), 16)]
+    assert not any(sessions(adv))
+    assert all(sessions(runs(320, 0.0)))
