@@ -86,6 +86,14 @@ def run(rounds_list, counts, samples_per_r, out):
             robust = {"threshold": rm.threshold, "margin": rm.margin,
                       "false_positive_rate_second_half": sum(1 for x in el[half:] if x > rm.threshold) /
                       max(1, len(el) - half)}
+            sess = {}
+            if half >= 32:
+                sm = verifier.calibrate_session(el[:half], 16, min_runs=min(30, half))
+                rest = el[half:]
+                verdicts = [verifier.verify_session([(i, 1, t, 1) for i, t in enumerate(rest[j:j + 16])], sm).accepted
+                            for j in range(0, len(rest) - 15, 16)]
+                sess = {"m": 16, "threshold": sm.threshold, "margin": sm.margin, "sessions": len(verdicts),
+                        "false_positive_rate_second_half": (1.0 - sum(verdicts) / len(verdicts)) if verdicts else None}
             skew, kurt = moments(el)
             entry = {"rounds": R, "n_attest": len(el), "wall_s": time.time() - t_start,
                      "elapsed_s": {"p50": verifier.percentile(el, 50), "p99": verifier.percentile(el, 99),
@@ -98,7 +106,7 @@ def run(rounds_list, counts, samples_per_r, out):
                      "calibrated_on_first_half": {"t_avg": model.t_avg, "sigma": model.sigma,
                                                   "threshold": model.threshold},
                      "false_positive_rate_second_half": fp, "normal_tail_2p5": verifier.normal_tail(2.5),
-                     "quantile_rule": quantile_fp, "robust_rule": robust,
+                     "quantile_rule": quantile_fp, "robust_rule": robust, "session_rule": sess,
                      "stalls": verifier.stall_estimate(el),
                      "thread_rounds_per_s_p50": n * R / verifier.percentile(el, 50),
                      "sum_of_partials_ok": sum_ok, "samples": samples,
