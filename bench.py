@@ -139,19 +139,13 @@ def cpu_oracle_rate(pool, nonce, base, rounds, warps, P):
     return len(warps) * 32 * rounds / dt, dt, sums
 
 
-def reference_region(nbytes, P):
-    """The workload's region for the oracle arm: the launched kernel's code + PCG64
-    fill when a GPU is there to ask which kernel that is (content does not change
-    the oracle's speed), else the fill alone."""
-    from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region
-    prefix = b""
-    try:
-        import torch
-        if torch.cuda.is_available() and nbytes <= (1 << 20):
-            prefix = launched_kernel_prefix(nbytes, pick_words=P)
-    except Exception:                                # no GPU / library: timing is content-independent
-        prefix = b""
-    return make_region(nbytes, prefix=prefix)
+def reference_region(nbytes):
+    """The workload's region for the oracle arm: the seeded PCG64 fill.  The oracle's
+    speed does not depend on the bytes, and the arm must not load the product
+    library, so the kernel-code prefix (which needs the library to name the
+    launched kernel) is left out here."""
+    from paper_2209_03125_b200.inputs import make_region
+    return make_region(nbytes)
 
 
 def run_reference(args):
@@ -161,7 +155,7 @@ def run_reference(args):
     import oracle
     nbytes, P, R, desc = CONFIGS[args.config]
     oracle.build()
-    region = reference_region(nbytes, P)
+    region = reference_region(nbytes)
     cores = len(os.sched_getaffinity(0))
     base = 0x7F00_0000_0000
     sample_warps = list(range(4 * cores))

@@ -19,13 +19,17 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
-    def start(self):
+    def start(self, wait_s=3.0):
+        """Start sampling; returns once the first sample is in (nvidia-smi takes a few
+        hundred ms to start), so even a sub-second timed region gets samples."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.first = threading.Event()
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            self.first.wait(wait_s)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -33,6 +37,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.first.set()
 
     def stop(self):
         if self.proc is None:
