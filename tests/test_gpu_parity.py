@@ -603,3 +603,28 @@ def test_single_bit_flips_change_the_gpu_checksum(dev):
             assert int(pw[w].item()) & M64 == oracle.warp_sum(0xF11B, flipped, d.data_ptr(), 64, w, 1)
         d.copy_(torch.from_numpy(region))
         assert ctx.attest(0xF11B, d, 64).checksum == base_cs
+
+
+@pytest.mark.parametrize("rounds", [0, 1, 17, 18, 19, 35, 36, 37, 18 * 7 + 5])
+def test_ilp2_round_loop_boundaries(dev, rounds):
+    """The c2a kernel runs UNROLL = 18 rounds of both lane states per trip and the
+    rest one by one (a10): every trip/remainder split around 0, 1, 18 and 36
+    rounds is bit-exact with the oracle (2 CTAs of 1024 threads -> ILP 2)."""
+    region = make_region(8192, fill_seed=rounds + 1)
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=2, threads=1024) as ctx:
+        res = ctx.attest(0xB0B + rounds, d, rounds)
+    assert res.ilp == 2 and res.placement == sage.SAGE_SMEM
+    assert res.checksum == oracle.attest(0xB0B + rounds, region, d.data_ptr(), rounds, 2, 1024, 1)
+
+
+@pytest.mark.parametrize("rounds", [0, 1, 2, 3, 7])
+def test_hybrid_round_loop_boundaries(dev, rounds):
+    """SAGE_HYBRID (UNROLL 2 + remainder) at small and odd round counts, region
+    256 KiB so 75% of the picks are staged and 25% read in place."""
+    region = make_region(256 << 10, fill_seed=rounds + 7)
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=2, threads=1024) as ctx:
+        res = ctx.attest(0x4B + rounds, d, rounds)
+    assert res.placement == sage.SAGE_HYBRID and res.ilp == 2
+    assert res.checksum == oracle.attest(0x4B + rounds, region, d.data_ptr(), rounds, 2, 1024, 1)
