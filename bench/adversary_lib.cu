@@ -29,6 +29,9 @@ struct Adv {
     Fn fn;
     int ilp;
     int memcopy;       // reads a copy at region + copy_delta while folding region's address
+    int stage = -1;    // shared-memory bytes staged: -1 = the whole region (SMEM), 0 = none
+                       // (GLOBAL), > 0 = a prefix of that many bytes (HYBRID)
+    int probe = 0;     // 1: a side experiment, not part of the adversary test
 };
 
 // <P, SMEM, STRADDLE, XS, UNROLL, ADDR, LD, EXTRA, COUNT, EVERY, ILP, PROBE, PAD, SYNC, FEXTRA, MEMCOPY>
@@ -58,6 +61,13 @@ const Adv kAdv[] = {
      sage_lab::sage_checksum_kernel<1, true, false, 16, ADV_ATK7_U, 4, 0, -1, false, 7, 2, 0, ADV_ATK7_PAD>, 2, 0},
     {"memory copy: stage a clean copy, fold the original address",
      sage_lab::sage_checksum_kernel<1, true, false, 16, 18, 4, 0, 0, false, 0, 2, 0, 7, 0, 0, 1>, 2, 1},
+    // side experiments (scripts/memcopy_probe.py): the memory-copy attack on the other
+    // placements -- GLOBAL (the product's P=1 GLOBAL kernel reading dp + delta) and
+    // SAGE_HYBRID (staged prefix and in-place part both from the copy)
+    {"memory copy on GLOBAL placement",
+     sage_lab::sage_checksum_kernel<1, false, true, 16, 16, 0, 0, 0, false, 0, 1, 0, 0, 0, 0, 1>, 1, 1, 0, 1},
+    {"memory copy on SAGE_HYBRID placement",
+     sage_lab::sage_checksum_kernel<1, true, false, 16, 2, 8, 0, 0, false, 0, 2, 0, 8, 0, 0, 1>, 2, 1, 196608, 1},
 };
 constexpr int kCount = sizeof(kAdv) / sizeof(kAdv[0]);
 
@@ -83,8 +93,9 @@ int ensure(int device) {
     if (cudaStreamCreateWithFlags(&g.stream, cudaStreamDefault) != cudaSuccess) return -4;
     if (cudaMalloc(&g.d_raw, 32) != cudaSuccess || cudaMallocHost(&g.h_raw, 32) != cudaSuccess) return -3;
     for (const Adv& a : kAdv)
-        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(a.fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 65536) != cudaSuccess)
+        if (a.stage != 0 && cudaFuncSetAttribute(reinterpret_cast<const void*>(a.fn),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 a.stage > 0 ? a.stage : 65536) != cudaSuccess)
             return -4;
     g.device = device;
     g.ready = true;
@@ -101,16 +112,22 @@ const char* adv_name(int k) { return (k >= 0 && k < kCount) ? kAdv[k].name : nul
 
 int adv_memcopy(int k) { return (k >= 0 && k < kCount) ? kAdv[k].memcopy : -1; }
 
-/* One attestation with adversary k at the c2a geometry (2 x SMs x 1024 logical
- * threads, P = 1, region staged in shared memory; region_bytes a power of two,
- * 16..65536).  copy_delta: for memory-copy adversaries, the byte offset of the clean
+int adv_probe(int k) { return (k >= 0 && k < kCount) ? kAdv[k].probe : -1; }
+
+/* One attestation with adversary k at full occupancy (2 x SMs x 1024 logical
+ * threads, P = 1; region_bytes a power of two >= 16, <= 64 KiB for kernels that
+ * stage the whole region).  copy_delta: for memory-copy adversaries, the byte offset of the clean
  * copy the kernel really reads (region + copy_delta); the folded address stays
  * `region`.  per_warp (device, may be NULL) gets the warp partials.  Returns 0, or
  * -1 bad argument, -3 allocation, -4 CUDA error. */
 int adv_attest(int k, int device, uint64_t nonce, const void* region, size_t region_bytes, uint32_t rounds,
                int64_t copy_delta, uint64_t* per_warp, uint64_t* checksum, uint64_t* elapsed_ns) {
     if (k < 0 || k >= kCount || region == nullptr || checksum == nullptr || elapsed_ns == nullptr) return -1;
-    if (region_bytes < 16 || region_bytes > 65536 || (region_bytes & (region_bytes - 1))) return -1;
+    if (region_bytes < 16 || (region_bytes & (region_bytes - 1))) return -1;
+    if (kAdv[k].stage < 0 && region_bytes > 65536) return -1;
+    const size_t dyn = kAdv[k].stage < 0 ? region_bytes
+                       : (kAdv[k].stage > 0 && region_bytes > size_t(kAdv[k].stage) ? size_t(kAdv[k].stage) : 0);
+    if (kAdv[k].stage > 0 && dyn == 0) return -1;      // HYBRID needs a region above its stage
     std::lock_guard<std::mutex> lock(g.mu);
     int rc = ensure(device);
     if (rc) return rc;
@@ -119,7 +136,7 @@ int adv_attest(int k, int device, uint64_t nonce, const void* region, size_t reg
     a.nonce = nonce;
     a.nc_mask = static_cast<uint32_t>(region_bytes / 4 - 1);
     a.rounds = rounds;
-    a.region_bytes = static_cast<uint32_t>(region_bytes);
+    a.region_bytes = static_cast<uint32_t>(dyn);
     a.raw = g.d_raw;
     a.per_warp = per_warp;
     a.copy_delta = copy_delta;
@@ -127,7 +144,7 @@ int adv_attest(int k, int device, uint64_t nonce, const void* region, size_t reg
     const int grid = 2 * g.sms / kAdv[k].ilp;
     const uint64_t t0 = now_ns();
     if (cudaMemsetAsync(g.d_raw, 0, 32, g.stream) != cudaSuccess) return -4;
-    kAdv[k].fn<<<grid, 1024, region_bytes, g.stream>>>(a);
+    kAdv[k].fn<<<grid, 1024, dyn, g.stream>>>(a);
     if (cudaGetLastError() != cudaSuccess) return -4;
     if (cudaMemcpyAsync(g.h_raw, g.d_raw, 32, cudaMemcpyDeviceToHost, g.stream) != cudaSuccess) return -4;
     if (cudaStreamSynchronize(g.stream) != cudaSuccess) return -4;

@@ -32,6 +32,8 @@ def load():
         L.adv_name.argtypes = [ctypes.c_int]
         L.adv_memcopy.restype = ctypes.c_int
         L.adv_memcopy.argtypes = [ctypes.c_int]
+        L.adv_probe.restype = ctypes.c_int
+        L.adv_probe.argtypes = [ctypes.c_int]
         L.adv_attest.restype = ctypes.c_int
         L.adv_attest.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t,
                                  ctypes.c_uint32, ctypes.c_int64, ctypes.c_void_p,
@@ -40,9 +42,12 @@ def load():
     return _lib
 
 
-def adversaries():
+def adversaries(probes=False):
+    """[(index, name, memory_copy)] of the adversary test's kernels (probes=True: the
+    side experiments of scripts/memcopy_probe.py instead)."""
     L = load()
-    return [(k, L.adv_name(k).decode(), bool(L.adv_memcopy(k))) for k in range(L.adv_count())]
+    return [(k, L.adv_name(k).decode(), bool(L.adv_memcopy(k))) for k in range(L.adv_count())
+            if bool(L.adv_probe(k)) == probes]
 
 
 def attest(k, nonce, region_ptr, nbytes, rounds, copy_delta=0, per_warp_ptr=None, device=0):
