@@ -68,6 +68,10 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 // attacker's schedule search: the c2a kernel + EXTRA injected every EVERY rounds
 #define VARE(U, PAD, EXTRA, EVERY) {"P1 smem xs16 unroll" #U " addr4 ILP2 PAD" #PAD " EXTRA" #EXTRA " EVERY" #EVERY, \
                   sage::sage_checksum_kernel<1, true, false, 16, U, 4, 0, EXTRA, false, EVERY, 2, 0, PAD>, 1, true, false, 2}
+// ... with the xorshift / pick-address lowering searched as well
+#define VAREX(XS, U, A, PAD, EXTRA, EVERY) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD " EXTRA" #EXTRA \
+                  " EVERY" #EVERY, sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, EXTRA, false, EVERY, 2, 0, PAD>, \
+                  1, true, false, 2}
 
 // round 2: hybrid (ADDR 8) with the global part's cache operator LD (1 no L1 allocation, 2 .cg)
 #define VARH8L(U, ST, PAD, LD) {"P1 hybrid8 unroll" #U " ILP2 stage" #ST " PAD" #PAD " LD" #LD, \

@@ -49,7 +49,7 @@ def grid(unrolls, pads, xss, addrs):
 def variant_name(pt, extra=0, every=0):
     xs, u, a, p = pt
     if extra:
-        return "P1 smem xs16 unroll%d addr4 ILP2 PAD%d EXTRA%d EVERY%d" % (u, p, extra, every)
+        return "P1 smem xs%d unroll%d addr%d ILP2 PAD%d EXTRA%d EVERY%d" % (xs, u, a, p, extra, every)
     return "P1 smem xs%d unroll%d addr%d ILP2 PAD%d" % pt
 
 
@@ -62,7 +62,7 @@ def build(points, binary, extra=0, every=0, reference=True):
             f.write("    VARZ(16, 18, 4, 7),\n")
         for xs, u, a, p in points:
             if extra:
-                f.write("    VARE(%d, %d, %d, %d),\n" % (u, p, extra, every))
+                f.write("    VAREX(%d, %d, %d, %d, %d, %d),\n" % (xs, u, a, p, extra, every))
             else:
                 f.write("    VARZ(%d, %d, %d, %d),\n" % (xs, u, a, p))
         inc = f.name
