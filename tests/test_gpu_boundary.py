@@ -110,3 +110,32 @@ def test_callers_current_device_is_restored(dev):
         ctx.query()
         ctx.kernel_symbol(4096)
     assert torch.cuda.current_device() == 0
+
+
+def test_timing_fields_are_consistent(dev):
+    """a13: the device span (%globaltimer, first CTA start -> last
+    CTA end) lies inside the host's t1 - t0 and agrees with CUDA events around the
+    same launch; max CTA cycles / device span is an SM clock (0.8-2.1 GHz); the
+    host overhead around the kernel (launch, 32-B readback) is well under a ms."""
+    region = make_region(8192)
+    d = torch.from_numpy(region).to(dev)
+    s = torch.cuda.Stream()
+    raw = torch.zeros(4, dtype=torch.int64, device=dev)
+    with sage.Context(stream=s) as ctx:
+        for _ in range(2):
+            res = ctx.attest(0x7117, d, 20_000)
+        assert 0 < res.device_ns <= res.elapsed_ns
+        assert res.elapsed_ns - res.device_ns < 1_000_000
+        ghz = res.cycles / res.device_ns
+        assert 0.8 < ghz < 2.1, ghz
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            raw.zero_()
+            e0.record(s)
+            ctx.attest_async(0x7117, d, 20_000, raw)
+            e1.record(s)
+        s.synchronize()
+        dec = sage.decode_raw(raw.cpu().tolist())
+        ev_ns = e0.elapsed_time(e1) * 1e6
+    assert dec.checksum == res.checksum
+    assert abs(dec.device_ns - ev_ns) < 0.02 * ev_ns, (dec.device_ns, ev_ns)
