@@ -220,7 +220,7 @@ def warm_up(ctx, region, R, nonces, warmup, steps, stream, dev, flush):
     return raw, ev, launches0
 
 
-def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms, args):
+def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms):
     """Secondary BASELINE configs timed in the same process (the driver's record of
     them): c2c (the paper's 524,288-B buffer, SAGE_HYBRID), c3p1 / c3p8 (256 MiB in
     HBM), each with kernel time, roofline fraction, DRAM traffic and clocks; plus
@@ -237,7 +237,8 @@ def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms, args):
         n = info.blocks * info.threads
         placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
         ceiling = random_gather_ceiling(nbytes) if nbytes > (1 << 20) else None
-        raw, ev, _ = warm_up(ctx, region, R, nonces, 2, 0, stream, dev, flush)
+        warm_up(ctx, region, R, nonces, 2, 0, stream, dev, flush)
+        raw = torch.zeros(EXTRA_STEPS, 4, dtype=torch.int64, device=dev)
         sampler = ClockSampler(dev.index).start()
         launches0 = ctx.launches
         kern = []
@@ -245,7 +246,7 @@ def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms, args):
             flush.fill_(k & 0xFF)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ctx.attest_async(nonces[2 + k], region, R, raw[0])
+            ctx.attest_async(nonces[2 + k], region, R, raw[k])
             e1.record(stream)
             kern.append((e0, e1))
         torch.cuda.synchronize(dev)
@@ -454,7 +455,7 @@ def run_ours(args):
         if ws == 1 and not args.no_extra and args.config == "c2a":
             del flush
             flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-            line["extra"] = run_extra({"device": local}, dev, stream, flush, peaks, peak_src, sms, args)
+            line["extra"] = run_extra({"device": local}, dev, stream, flush, peaks, peak_src, sms)
         print(json.dumps(line), flush=True)
     ctx.close()
     if ws > 1:

@@ -2,7 +2,6 @@
 launches (so the region can carry that kernel's own code),
 validation before the host-region staging buffer is touched, stream ordering
 of the context-owned stream, and the caller's current device."""
-import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
