@@ -402,7 +402,30 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
         static_assert(P == 1, "ADDR 8 is the P = 1 hybrid form");
-        if constexpr (LD == 1)        // round 2: global part without L1 allocation
+        if constexpr (LD == 5 || LD == 6) {
+            // round 2: keep a fixed window of the in-place part in L1 -- chunks in
+            // [staged, staged + persist_bytes) load with .L1::evict_last, the rest with
+            // .L1::no_allocate (LD 5) or .L1::evict_first (LD 6)
+            const uint32_t win = static_cast<uint32_t>(args.persist_bytes) / args.four_p + staged_chunks;
+            if constexpr (LD == 5)
+                asm volatile("{\n\t.reg .pred ps, pw, pn;\n\t"
+                             "setp.lt.u32 ps, %1, %2;\n\t"
+                             "setp.lt.u32 pw, %1, %5;\n\t"
+                             "setp.ge.and.u32 pn, %1, %2, pw;\n\t"
+                             "@ps ld.shared.b32 %0, [%3];\n\t"
+                             "@pn ld.global.nc.L1::evict_last.b32 %0, [%4];\n\t"
+                             "@!pw ld.global.nc.L1::no_allocate.b32 %0, [%4];\n\t}"
+                             : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr), "r"(win));
+            else
+                asm volatile("{\n\t.reg .pred ps, pw, pn;\n\t"
+                             "setp.lt.u32 ps, %1, %2;\n\t"
+                             "setp.lt.u32 pw, %1, %5;\n\t"
+                             "setp.ge.and.u32 pn, %1, %2, pw;\n\t"
+                             "@ps ld.shared.b32 %0, [%3];\n\t"
+                             "@pn ld.global.nc.L1::evict_last.b32 %0, [%4];\n\t"
+                             "@!pw ld.global.nc.L1::evict_first.b32 %0, [%4];\n\t}"
+                             : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr), "r"(win));
+        } else if constexpr (LD == 1)        // round 2: global part without L1 allocation
             asm volatile("{\n\t.reg .pred p;\n\t"
                          "setp.lt.u32 p, %1, %2;\n\t"
                          "@p ld.shared.b32 %0, [%3];\n\t"
