@@ -628,3 +628,20 @@ def test_hybrid_round_loop_boundaries(dev, rounds):
         res = ctx.attest(0x4B + rounds, d, rounds)
     assert res.placement == sage.SAGE_HYBRID and res.ilp == 2
     assert res.checksum == oracle.attest(0x4B + rounds, region, d.data_ptr(), rounds, 2, 1024, 1)
+
+
+@pytest.mark.parametrize("blocks,threads", [(1, 64), (2, 1024)])
+def test_zero_seed_threads(dev, blocks, threads):
+    """I2 on the GPU: SplitMix64's only zero output is sm(0), reached by thread g when
+    nonce = -(g+1)*G (mod 2^64); that thread's xorshift state must start at G instead
+    of 0 (a zero state would stay zero forever).  Nonces that zero the seeds of
+    threads 0, 1, 33 and the last one, in the ILP-1 and ILP-2 kernels."""
+    G = 0x9E3779B97F4A7C15
+    region = make_region(4096, fill_seed=99)
+    d, _keep = to_dev(region, dev)
+    n = blocks * threads
+    with sage.Context(blocks=blocks, threads=threads) as ctx:
+        for g in (0, 1, 33, n - 1):
+            nonce = (-(g + 1) * G) & M64
+            res = ctx.attest(nonce, d, 50)
+            assert res.checksum == oracle.attest(nonce, region, d.data_ptr(), 50, blocks, threads, 1), g
