@@ -1,6 +1,7 @@
 """SAGE's security claim on B200, driver-verified (Table 1 Exp 1
 vs Exp 2): the product's c2a attestation (sage_attest) is
-interleaved run by run with adversary kernels from the test-only
+interleaved run by run (96 passes of 5 honest runs and one run of each
+adversary) with adversary kernels from the test-only
 bench/libsage_adv.so -- one IMAD per round on the product's schedule and on the
 attacker's own searched schedules (scripts/schedule_search.py --extra), one ALU
 op per 18 rounds, one IMAD per 7 rounds (about one per paper iteration of 428
@@ -32,7 +33,7 @@ from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, no
 
 pytestmark = pytest.mark.gpu
 R = 100_000
-PASSES, HONEST_PER_PASS, CALIB, SESSION = 96, 3, 96, 16
+PASSES, HONEST_PER_PASS, CALIB, SESSION = 96, 5, 96, 16
 FASTEST = "+1 IMAD / round (attacker-searched schedule)"     # within single-run noise
 M64 = (1 << 64) - 1
 
