@@ -122,6 +122,18 @@ def roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, workload,
     return rf
 
 
+def cpu_model():
+    """The host CPU's model name (/proc/cpuinfo), for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -174,7 +186,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "config": {"workload": args.config, "desc": desc, "region_bytes": nbytes, "P": P,
                                               "rounds": R},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -446,7 +459,7 @@ def run_ours(args):
             with oracle.WarpPool(host, 1) as pool1:             # one core, a smaller sample
                 rate1, dt1, sums1 = cpu_oracle_rate(pool1, 0x1234, region.data_ptr(), R, sample[:4], P)
             ok = all(sums[w] == parts[w] for w in sample) and (sum(parts) & (2**64 - 1)) == dbg.checksum
-            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                                     "sample": "%d warps x %d threads x %d rounds of this workload (%.1f s)"
                                               % (len(sample), 32, R, dt),
                                     "single_core_value": rate1,
