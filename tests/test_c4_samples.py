@@ -11,9 +11,11 @@ import pytest
 
 import oracle
 
-DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01")
-PATHS = [os.path.join(DIR, f) for f in ("scs2/c4_timing.json", "scs2/c4_timing_full.json", "ilp2/c4_timing_full.json",
-                                         "final/c4_timing_full.json", "final/c4_timing_full_v2.json")]
+PROFILES = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+PATHS = [os.path.join(PROFILES, "r01", f) for f in ("scs2/c4_timing.json", "scs2/c4_timing_full.json",
+                                                    "ilp2/c4_timing_full.json", "final/c4_timing_full.json",
+                                                    "final/c4_timing_full_v2.json")] + \
+    [os.path.join(PROFILES, "r02", "final", "c4_timing.json")]
 
 
 @pytest.mark.parametrize("path", PATHS)
