@@ -175,7 +175,9 @@ def test_session_model_closed_form_and_checks():
     xs = [100.0 + d for d in (-2, -1, 0, 1, 2)] * 6          # median 100, MAD 1
     m = V.calibrate_session(xs, m=16, k=6.0, min_margin=0.0)
     assert m.median == 100.0 and m.sigma_r == pytest.approx(1.4826)
-    assert m.margin == pytest.approx(6 * 1.2533 * 1.4826 / (4 * 100.0))
+    # median: sqrt(q (1 - q)) / phi(0) = sqrt(pi / 2) = 1.2533...
+    assert m.margin == pytest.approx(6 * math.sqrt(math.pi / 2) * 1.4826 / (4 * 100.0))
+    assert m.threshold == pytest.approx(100.0 * (1 + m.margin))
     assert V.calibrate_session(xs, m=16, min_margin=0.5).margin == 0.5
     runs = [(n, 7, 100.0, 7) for n in range(16)]
     assert V.verify_session(runs, m).accepted
@@ -212,3 +214,37 @@ def test_session_median_separates_a_small_shift_that_single_runs_cannot():
                           for j in range(0, len(t), 16)]
     assert not any(sessions(adv))
     assert all(sessions(runs(320, 0.0)))
+
+
+def test_session_quantile_rule_bounds_partial_cheating():
+    """calibrate_session(q=13/15): the 14th smallest of 16 run times (linear
+    interpolation puts q = 13/15 exactly on it).  Its standard error
+    sigma * sqrt(q(1-q)) / (phi(z_q) sqrt(m)) is checked in closed form (z_{13/15} =
+    1.11077); on synthetic B200-like times an attacker +0.07% slower in 5 of 16
+    challenges passes the median rule but fails the q = 13/15 rule, while honest
+    sessions with two paused runs pass both."""
+    q = 13 / 15
+    z = 1.110771
+    phi = math.exp(-z * z / 2) / math.sqrt(2 * math.pi)
+    xs = [100.0 + d for d in (-2, -1, 0, 1, 2)] * 6
+    mq = V.calibrate_session(xs, m=16, q=q, min_margin=0.0)
+    assert mq.margin == pytest.approx(6 * 1.4826 * math.sqrt(q * (1 - q)) / (phi * 4) / 100.0, rel=1e-6)
+    assert mq.quantile == V.percentile(xs, 100 * q)
+    assert V.percentile(list(range(16)), 100 * q) == pytest.approx(13.0)
+    rng = np.random.default_rng(9)
+    T, s = 0.0538, 0.00013 * 0.0538
+    cal = T + rng.normal(0, s, 200)
+    med_rule, q_rule = V.calibrate_session(cal, 16), V.calibrate_session(cal, 16, q=q)
+
+    def verdicts(t, model):
+        return [V.verify_session([(i, 1, x, 1) for i, x in enumerate(t[j:j + 16])], model).accepted
+                for j in range(0, len(t), 16)]
+    honest = T + rng.normal(0, s, 320)
+    honest[::16] += 0.03 * T                        # one paused run per session
+    honest[5::16] += 0.03 * T                       # and a second one
+    assert all(verdicts(honest, med_rule)) and all(verdicts(honest, q_rule))
+    partial = T + rng.normal(0, s, 320)
+    for j in range(0, 320, 16):
+        partial[j:j + 5] += 0.0007 * T              # cheating in 5 of 16 challenges
+    assert all(verdicts(partial, med_rule))
+    assert not any(verdicts(partial, q_rule))
