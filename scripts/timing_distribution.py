@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+from bench.clocks import ClockSampler  # noqa: E402
 from paper_2209_03125_b200 import sage, verifier  # noqa: E402
 from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, nonces  # noqa: E402
 
@@ -60,6 +61,7 @@ def run(rounds_list, counts, samples_per_r, out):
             for k in range(3):                                   # warm-up
                 ctx.attest(ns[k] ^ 0xFFFF, region, R)
             el, dv, cyc, samples, sum_ok = [], [], [], [], 0
+            clk = ClockSampler(torch.cuda.current_device()).start()
             t_start = time.time()
             for k, nonce in enumerate(ns):
                 res = ctx.attest_debug(nonce, region, R, pw)
@@ -72,6 +74,8 @@ def run(rounds_list, counts, samples_per_r, out):
                     w = (nonce >> 17) % (n // 32)
                     samples.append({"nonce": nonce, "checksum": res.checksum, "warp": int(w),
                                     "warp_partial": int(parts[w]) & M64})
+            wall_s = time.time() - t_start
+            clocks = clk.stop()
             half = len(el) // 2
             model = verifier.calibrate(el[:half], min_runs=min(30, half))
             fp = sum(1 for x in el[half:] if x > model.threshold) / max(1, len(el) - half)
@@ -95,7 +99,7 @@ def run(rounds_list, counts, samples_per_r, out):
                 sess = {"m": 16, "threshold": sm.threshold, "margin": sm.margin, "sessions": len(verdicts),
                         "false_positive_rate_second_half": (1.0 - sum(verdicts) / len(verdicts)) if verdicts else None}
             skew, kurt = moments(el)
-            entry = {"rounds": R, "n_attest": len(el), "wall_s": time.time() - t_start,
+            entry = {"rounds": R, "n_attest": len(el), "wall_s": wall_s, "clocks": clocks,
                      "elapsed_s": {"p50": verifier.percentile(el, 50), "p99": verifier.percentile(el, 99),
                                    "min": min(el), "max": max(el), "mean": model_all.t_avg, "sigma": model_all.sigma,
                                    "threshold_2p5sigma": model_all.threshold, "skew": skew, "excess_kurtosis": kurt,
@@ -110,9 +114,12 @@ def run(rounds_list, counts, samples_per_r, out):
                      "stalls": verifier.stall_estimate(el),
                      "thread_rounds_per_s_p50": n * R / verifier.percentile(el, 50),
                      "sum_of_partials_ok": sum_ok, "samples": samples,
-                     "elapsed_ns_all": [int(round(x * 1e9)) for x in el]}
+                     "elapsed_ns_all": [int(round(x * 1e9)) for x in el],
+                     "device_ns_all": [int(round(x * 1e9)) for x in dv], "cycles_all": cyc}
             result["per_R"].append(entry)
-            print(json.dumps({k: v for k, v in entry.items() if k not in ("samples", "elapsed_ns_all")}), flush=True)
+            with open(out, "w") as f:                           # after every R: a cut-off run keeps what it has
+                json.dump(result, f, indent=1)
+            print(json.dumps({k: v for k, v in entry.items() if k not in ("samples", "elapsed_ns_all", "device_ns_all", "cycles_all")}), flush=True)
     with open(out, "w") as f:
         json.dump(result, f, indent=1)
 
