@@ -31,7 +31,7 @@ from bench.clocks import ClockSampler  # noqa: E402
 METRIC = "checksum rounds/s and checksummed GB/s per B200 (1/2/4/8 GPU); p99 attest time"
 UNIT = "thread-rounds/s"
 ATTEST_SAMPLES, ATTEST_BUDGET_S = 200, 15.0   # attest_ms distribution: up to 200 runs / ~15 s
-EXTRA_CONFIGS, EXTRA_STEPS = ("c2c", "c3p1", "c3p8"), 5   # timed beside c2a in the same run ("extra")
+EXTRA_CONFIGS, EXTRA_STEPS = ("c2c", "c2cp4", "c2cp8", "c3p1", "c3p8"), 5   # timed beside c2a in the same run ("extra")
 CPU_SAMPLE_S = 20.0          # cpu_baseline sizing target (the one-warp-per-core calibration pass
                              # overestimates the per-warp cost ~2x, so the timed sample runs ~10 s)
 
@@ -46,6 +46,8 @@ CONFIGS = {
     "c2b": (65536, 1, 100_000, "full occupancy, 64 KiB SMEM region, 1e5 rounds"),
     "c2c": (524288, 1, 100_000, "full occupancy, the paper's 512 KiB buffer (P:690): first 192 KiB staged in SMEM, "
                                    "the rest read from L2 (SAGE_HYBRID), 1e5 rounds"),
+    "c2cp4": (524288, 4, 100_000, "full occupancy, the paper's 512 KiB buffer (P:690), P=4 (16-B picks), 1e5 rounds"),
+    "c2cp8": (524288, 8, 100_000, "full occupancy, the paper's 512 KiB buffer (P:690), P=8 (32-B picks), 1e5 rounds"),
     "c3p1": (256 << 20, 1, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=1, 1e4 rounds"),
     "c3p4": (256 << 20, 4, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=4, 1e4 rounds"),
     "c3p8": (256 << 20, 8, 10_000, "full occupancy, 256 MiB HBM region (GLOBAL), P=8, 1e4 rounds"),
@@ -235,7 +237,8 @@ def warm_up(ctx, region, R, nonces, warmup, steps, stream, dev, flush):
 
 def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms):
     """Secondary BASELINE configs timed in the same process (the driver's record of
-    them): c2c (the paper's 524,288-B buffer, SAGE_HYBRID), c3p1 / c3p8 (256 MiB in
+    them): c2c (the paper's 524,288-B buffer, SAGE_HYBRID) and c2cp4 / c2cp8 (the same
+    buffer with 16- / 32-B picks), c3p1 / c3p8 (256 MiB in
     HBM), each with kernel time, roofline fraction, DRAM traffic and clocks; plus
     the attestation wall-time distribution at R = 10^4 (config 4's shortest)."""
     import torch
@@ -497,7 +500,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=0, help="override the workload's round count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs (c2c, c3p1, c3p8, R=1e4)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs (c2c, c2cp4, c2cp8, c3p1, c3p8, R=1e4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

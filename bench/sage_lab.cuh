@@ -444,6 +444,33 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                      "@!p ld.global.nc.b32 %0, [%4];\n\t}"
                      : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 10) {
+        // round 2: the ADDR 8 hybrid (FMA-pipe addressing, R6 bracket folded into the
+        // chunk-offset IMAD) for P = 4 / 8: LDS.128 x P/4 from the staged prefix, one
+        // 128 / 256-bit LDG from global
+        static_assert(P == 4 || P == 8, "ADDR 10 is the P = 4 / 8 hybrid form");
+        const uint32_t saddr = i * args.four_p + smem_u32(smem_words);
+        const uint64_t gaddr = static_cast<uint64_t>(i) * args.four_p + base;
+        const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
+        const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        if constexpr (P == 4) {
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %4, %5;\n\t"
+                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%6];\n\t"
+                         "@!p ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%7];\n\t}"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3])
+                         : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        } else {
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %8, %9;\n\t"
+                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%10];\n\t"
+                         "@p ld.shared.v4.b32 {%4,%5,%6,%7}, [%10+16];\n\t"
+                         "@!p ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%11];\n\t}"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7])
+                         : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        }
+        t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 9) {
         // round 2: hybrid over a 2-CTA cluster.  CTA rank k stages bytes [k*S, (k+1)*S) of
         // the region (S = region_bytes); a pick below 2S is read from the owner's shared

@@ -61,8 +61,8 @@ def test_our_arm_one_gpu():
     assert line["config"]["kernel"].startswith("_ZN4sage20sage_checksum_kernel")
     # the secondary configs timed in the same process
     ex = line["extra"]
-    assert set(ex) == {"c2c", "c3p1", "c3p8", "attest_ms_r1e4"}
-    for name in ("c2c", "c3p1", "c3p8"):
+    assert set(ex) == {"c2c", "c2cp4", "c2cp8", "c3p1", "c3p8", "attest_ms_r1e4"}
+    for name in ("c2c", "c2cp4", "c2cp8", "c3p1", "c3p8"):
         e = ex[name]
         assert e["steps"] == 5 and e["gpu_launches"] == 5 and e["kernel_ms"]["mean"] > 0
         assert 0 < e["roofline"]["frac"] <= 1 and {"sm_mhz", "reasons"} <= set(e["clocks"])

@@ -514,22 +514,26 @@ def test_ilp2_placements_straddling_region_run_global(dev, nbytes):
     del big
 
 
-def test_paper_buffer_full_occupancy_sampled(dev):
-    """c2c as bench.py times it: the paper's 524,288-B buffer at full
-    occupancy (SAGE_HYBRID), 10^5 rounds; sum consistency plus sampled warps."""
-    region = make_region(512 << 10, prefix=launched_kernel_prefix(512 << 10))
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_paper_buffer_full_occupancy_sampled(dev, P):
+    """c2c / c2cp4 / c2cp8 as bench.py times them: the paper's 524,288-B buffer
+     at full occupancy, 10^5 rounds (P = 1, 4, 8); sum
+    consistency plus sampled warps.  P = 1 runs SAGE_HYBRID."""
+    region = make_region(512 << 10, prefix=launched_kernel_prefix(512 << 10, pick_words=P))
     d, _keep = to_dev(region, dev)
     R = 100_000
-    with sage.Context() as ctx:
+    with sage.Context(pick_words=P) as ctx:
         info = ctx.query()
         n = info.blocks * info.threads
         pw = torch.zeros(n // 32, dtype=torch.int64, device=dev)
-        res = ctx.attest_debug(0xC2C, d, R, pw)
-    assert res.placement == sage.SAGE_HYBRID
+        res = ctx.attest_debug(0xC2C + P, d, R, pw)
+        assert res.placement == ctx.placement_for(512 << 10)
+    if P == 1:
+        assert res.placement == sage.SAGE_HYBRID
     parts = [int(v) & M64 for v in pw.cpu().tolist()]
     assert sum(parts) & M64 == res.checksum
     for w in (0, 1, n // 64, n // 32 - 1):
-        assert parts[w] == oracle.warp_sum(0xC2C, region, d.data_ptr(), R, w, 1), w
+        assert parts[w] == oracle.warp_sum(0xC2C + P, region, d.data_ptr(), R, w, P), w
 
 
 def test_no_other_kernel_runs_beside_an_attestation(dev):
