@@ -401,7 +401,7 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         const uint64_t gaddr = static_cast<uint64_t>(i) * args.four_p + (MEMCOPY ? base + args.copy_delta : base);
         const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
-        static_assert(P == 1, "ADDR 8 is the P = 1 hybrid form");
+        static_assert(P == 1 || LD == 0, "ADDR 8 cache-operator variants are P = 1 forms");
         if constexpr (LD == 5 || LD == 6) {
             // round 2: keep a fixed window of the in-place part in L1 -- chunks in
             // [staged, staged + persist_bytes) load with .L1::evict_last, the rest with
@@ -437,12 +437,28 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                          "@p ld.shared.b32 %0, [%3];\n\t"
                          "@!p ld.global.cg.b32 %0, [%4];\n\t}"
                          : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
-        else
+        else if constexpr (P == 1)
         asm volatile("{\n\t.reg .pred p;\n\t"
                      "setp.lt.u32 p, %1, %2;\n\t"
                      "@p ld.shared.b32 %0, [%3];\n\t"
                      "@!p ld.global.nc.b32 %0, [%4];\n\t}"
                      : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        else if constexpr (P == 4)    // the product's P = 4 SAGE_HYBRID form (= ADDR 10, session 2)
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %4, %5;\n\t"
+                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%6];\n\t"
+                         "@!p ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%7];\n\t}"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3])
+                         : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        else
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %8, %9;\n\t"
+                         "@p ld.shared.v4.b32 {%0,%1,%2,%3}, [%10];\n\t"
+                         "@p ld.shared.v4.b32 {%4,%5,%6,%7}, [%10+16];\n\t"
+                         "@!p ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%11];\n\t}"
+                         : "=r"(d.w[0]), "=r"(d.w[1]), "=r"(d.w[2]), "=r"(d.w[3]),
+                           "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7])
+                         : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 10) {
         // round 2: the ADDR 8 hybrid (FMA-pipe addressing, R6 bracket folded into the

@@ -54,6 +54,12 @@ constexpr size_t kSmemRegionMaxIlp2 = 128 * 1024;
 // <= 1 MiB: 61.7 / 75.6 / 18.1 ms (R = 2e4) vs 64.0 / 93.7 / 18.8 ms GLOBAL at
 // 256 KiB / 512 KiB / 1 MiB.
 constexpr size_t kHybridStage = 192 * 1024, kHybridRegionMax = 1024 * 1024;
+// P = 4 (16-B picks) takes SAGE_HYBRID from 512 KiB: 75.8 vs 89.1 ms GLOBAL at the
+// paper's 524,288-B buffer (R = 1e5), 17.5-18.4 vs 18.9 ms at 1 MiB (R = 2e4); at
+// 256 KiB the fully-read-in-place form is faster (65.6-72.5 vs 69.4 ms),
+// profiles/r02/c2c48/.  P = 8 stays GLOBAL: its staged picks (two LDS.128 each) are
+// slower than L1 (117.3 vs 113.8 ms at 512 KiB).
+constexpr size_t kHybridRegionMinP4 = 512 * 1024;
 
 using KernelFn = void (*)(const sage::KernelArgs);
 
@@ -98,11 +104,16 @@ uint32_t ilp_for(uint32_t P, bool smem, bool straddle, uint32_t blocks, uint32_t
     return (P == 1 && smem && !straddle && threads == 1024 && blocks % kIlpSmem == 0) ? kIlpSmem : 1;
 }
 
-// SAGE_HYBRID kernel: ILP 2 as above, addressing on the FMA pipe (ADDR 8), 2 unrolled
-// rounds, 8 reserved registers (64 in all).
-constexpr int kHybridUnroll = 2, kHybridPad = 8;
-KernelFn hybrid_kernel() {
-    return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 8, false, kIlpSmem, kHybridPad>;
+// SAGE_HYBRID kernels: ILP 2 as above, addressing on the FMA pipe (ADDR 8).  P = 1: 2
+// unrolled rounds, 8 reserved registers (64 in all); P = 4: 1 round per trip, no
+// reservation (60 registers, allocated as 64).  P = 8 has none (see kHybridRegionMinP4).
+constexpr int kHybridUnroll = 2, kHybridPad = 8, kHybridUnrollP4 = 1, kHybridPadP4 = 0;
+KernelFn hybrid_kernel(uint32_t P) {
+    switch (P) {
+        case 1: return sage::sage_checksum_kernel<1, true, false, 16, kHybridUnroll, 8, false, kIlpSmem, kHybridPad>;
+        case 4: return sage::sage_checksum_kernel<4, true, false, 16, kHybridUnrollP4, 8, false, kIlpSmem, kHybridPadP4>;
+        default: return nullptr;
+    }
 }
 
 template <int P>
@@ -235,18 +246,24 @@ int validate(const sage_ctx* c, const void* region, size_t bytes, uint64_t round
 // SAGE_AUTO: SMEM when the region fits at 2 CTAs/SM, except P = 8, whose
 // random 32-B picks conflict heavily in shared-memory banks and run faster
 // from L1 (measured: 1510 vs 1843 cycles per round at 8 KiB).
-// The geometry of the ILP 2 kernels (c2a SMEM and SAGE_HYBRID).
+// The geometry of the ILP 2 kernels: one CTA of 1024 threads per SM (an even block
+// count of 1024-thread blocks).  The c2a SMEM kernel is P = 1 only; SAGE_HYBRID has
+// P = 1 and P = 4 forms.
+bool ilp2_geometry(const sage_ctx* c) { return c->threads == 1024 && c->blocks % kIlpSmem == 0; }
 bool hybrid_geometry(const sage_ctx* c) {
-    return c->pick_words == 1 && c->threads == 1024 && c->blocks % kIlpSmem == 0;
+    return (c->pick_words == 1 || c->pick_words == 4) && ilp2_geometry(c);
 }
 
-size_t smem_region_max(const sage_ctx* c) { return hybrid_geometry(c) ? kSmemRegionMaxIlp2 : kSmemRegionMax; }
+size_t smem_region_max(const sage_ctx* c) {
+    return c->pick_words == 1 && ilp2_geometry(c) ? kSmemRegionMaxIlp2 : kSmemRegionMax;
+}
 
 uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
     if (c->placement != SAGE_AUTO) return c->placement;
     if (c->pick_words == 8) return SAGE_GLOBAL;
     if (bytes <= smem_region_max(c)) return SAGE_SMEM;
-    if (bytes <= kHybridRegionMax && hybrid_geometry(c)) return SAGE_HYBRID;
+    if (bytes <= kHybridRegionMax && hybrid_geometry(c) && (c->pick_words == 1 || bytes >= kHybridRegionMinP4))
+        return SAGE_HYBRID;
     return SAGE_GLOBAL;
 }
 
@@ -281,7 +298,7 @@ int plan_launch(const sage_ctx* c, const void* region, size_t bytes, bool counti
     uint32_t placement = counting ? SAGE_GLOBAL : choose_placement(c, bytes);
     if (placement == SAGE_SMEM && bytes > smem_region_max(c))
         return fail(SAGE_EUNSUPPORTED, "SAGE_SMEM forced but the region exceeds %s",
-                    hybrid_geometry(c) ? "128 KiB" : "64 KiB");
+                    smem_region_max(c) > kSmemRegionMax ? "128 KiB" : "64 KiB");
     const uint64_t lo = reinterpret_cast<uint64_t>(region);
     const bool straddle = (lo >> 32) != ((lo + bytes - 1) >> 32);
     if (placement == SAGE_SMEM && straddle && bytes > kSmemRegionMax) {
@@ -293,7 +310,7 @@ int plan_launch(const sage_ctx* c, const void* region, size_t bytes, bool counti
     }
     if (placement == SAGE_HYBRID && (!hybrid_geometry(c) || straddle)) {
         if (c->placement == SAGE_HYBRID)
-            return fail(SAGE_EUNSUPPORTED, "SAGE_HYBRID needs P=1, 1024-thread blocks, an even block count and a "
+            return fail(SAGE_EUNSUPPORTED, "SAGE_HYBRID needs P=1 or 4, 1024-thread blocks, an even block count and a "
                                            "region inside one 4 GiB window%s");
         placement = SAGE_GLOBAL;                    // AUTO: a straddling region runs GLOBAL
     }
@@ -303,7 +320,7 @@ int plan_launch(const sage_ctx* c, const void* region, size_t bytes, bool counti
     KernelFn fn = counting ? counting_kernel_for(c->pick_words) : kernel_for(c->pick_words, smem, straddle, ilp);
     if (hybrid) {
         ilp = kIlpSmem;
-        fn = hybrid_kernel();
+        fn = hybrid_kernel(c->pick_words);
     }
     if (fn == nullptr) return fail(SAGE_EINVAL, "pick_words must be 1, 4 or 8%s");
     out->fn = fn;
@@ -398,7 +415,8 @@ int prepare_kernels(const sage_ctx* c) {
     int rc = ensure_dyn_smem(c->device, kernel_for(c->pick_words, true, false, ilp),
                              static_cast<int>(smem_region_max(c)));
     if (rc == SAGE_OK) rc = ensure_dyn_smem(c->device, kernel_for(c->pick_words, true, true), static_cast<int>(kSmemRegionMax));
-    if (rc == SAGE_OK && hybrid_geometry(c)) rc = ensure_dyn_smem(c->device, hybrid_kernel(), static_cast<int>(kHybridStage));
+    if (rc == SAGE_OK && hybrid_geometry(c))
+        rc = ensure_dyn_smem(c->device, hybrid_kernel(c->pick_words), static_cast<int>(kHybridStage));
     return rc;
 }
 

@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 # product template sage_checksum_kernel<P, SMEM, STRADDLE, XS, UNROLL, ADDR, COUNT, ILP, PAD>
 C2A = "_ZN4sage20sage_checksum_kernelILi1ELb1ELb0ELi16ELi18ELi4ELb0ELi2ELi7EEEvNS_10KernelArgsE"
 HYBRID = "_ZN4sage20sage_checksum_kernelILi1ELb1ELb0ELi16ELi2ELi8ELb0ELi2ELi8EEEvNS_10KernelArgsE"
+HYBRID_P4 = "_ZN4sage20sage_checksum_kernelILi4ELb1ELb0ELi16ELi1ELi8ELb0ELi2ELi0EEEvNS_10KernelArgsE"
 GLOBAL_P1 = "_ZN4sage20sage_checksum_kernelILi1ELb0ELb1ELi16ELi16ELi0ELb0ELi1ELi0EEEvNS_10KernelArgsE"
 GLOBAL_P8 = "_ZN4sage20sage_checksum_kernelILi8ELb0ELb1ELi16ELi1ELi0ELb0ELi1ELi0EEEvNS_10KernelArgsE"
 SMEM_ILP1 = "_ZN4sage20sage_checksum_kernelILi1ELb1ELb0ELi16ELi32ELi4ELb0ELi1ELi0EEEvNS_10KernelArgsE"
@@ -32,6 +33,7 @@ def dev():
 @pytest.mark.parametrize("cfg,nbytes,symbol,placement,ilp", [
     ({}, 8192, C2A, sage.SAGE_SMEM, 2),                       # c2a (bench default)
     ({}, 512 << 10, HYBRID, sage.SAGE_HYBRID, 2),             # c2c, the paper's buffer
+    ({"pick_words": 4}, 512 << 10, HYBRID_P4, sage.SAGE_HYBRID, 2),   # c2cp4
     ({}, 256 << 20, GLOBAL_P1, sage.SAGE_GLOBAL, 1),          # c3
     ({"pick_words": 8}, 256 << 20, GLOBAL_P8, sage.SAGE_GLOBAL, 1),
     ({"blocks": 2, "threads": 64}, 4096, SMEM_ILP1, sage.SAGE_SMEM, 1),   # smoke()

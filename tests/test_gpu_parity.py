@@ -468,9 +468,48 @@ def test_hybrid_placement_bit_exact(dev, nbytes):
     assert out[sage.SAGE_AUTO].checksum == out[sage.SAGE_GLOBAL].checksum == want
 
 
+@pytest.mark.parametrize("nbytes,auto", [(256 << 10, sage.SAGE_GLOBAL), (512 << 10, sage.SAGE_HYBRID),
+                                         (1 << 20, sage.SAGE_HYBRID)])
+def test_hybrid_p4_bit_exact(dev, nbytes, auto):
+    """The P = 4 SAGE_HYBRID form (16-B picks; LDS.128 from the staged 192 KiB,
+    LDG.128 in place): SAGE_AUTO takes it from 512 KiB to 1 MiB (GLOBAL below, where
+    reading in place is faster); forced, auto and GLOBAL placements are bit-exact with
+    the oracle."""
+    region = make_region(nbytes, prefix=launched_kernel_prefix(nbytes, blocks=2, threads=1024, pick_words=4),
+                         fill_seed=nbytes + 4)
+    d, _keep = to_dev(region, dev, align_offset=16)
+    out = {}
+    for placement in (sage.SAGE_AUTO, sage.SAGE_HYBRID, sage.SAGE_GLOBAL):
+        with sage.Context(blocks=2, threads=1024, pick_words=4, placement=placement) as ctx:
+            out[placement] = ctx.attest(0x48B4, d, 200)
+    assert out[sage.SAGE_AUTO].placement == auto
+    assert out[sage.SAGE_HYBRID].placement == sage.SAGE_HYBRID and out[sage.SAGE_HYBRID].ilp == 2
+    assert out[sage.SAGE_GLOBAL].placement == sage.SAGE_GLOBAL
+    want = oracle.attest(0x48B4, region, d.data_ptr(), 200, 2, 1024, 4)
+    assert out[sage.SAGE_AUTO].checksum == out[sage.SAGE_HYBRID].checksum == out[sage.SAGE_GLOBAL].checksum == want
+
+
+@pytest.mark.parametrize("rounds", [0, 1, 2, 3, 37])
+def test_hybrid_p4_forced_small_region(dev, rounds):
+    """Forced P = 4 SAGE_HYBRID on a 64 KiB region stages all of it (every pick an
+    LDS.128), at the round-loop edge cases; P = 8 has no HYBRID form."""
+    region = make_region(64 << 10, fill_seed=4 + rounds)
+    d, _keep = to_dev(region, dev)
+    with sage.Context(blocks=4, threads=1024, pick_words=4, placement=sage.SAGE_HYBRID) as ctx:
+        res = ctx.attest(0x4A + rounds, d, rounds)
+    assert res.placement == sage.SAGE_HYBRID and res.ilp == 2
+    assert res.checksum == oracle.attest(0x4A + rounds, region, d.data_ptr(), rounds, 4, 1024, 4)
+    with sage.Context(blocks=2, threads=1024, pick_words=8, placement=sage.SAGE_HYBRID) as ctx:
+        with pytest.raises(sage.SageError) as e:
+            ctx.attest(5, d, 10)
+        assert e.value.code == sage.SAGE_EUNSUPPORTED
+    with sage.Context(blocks=2, threads=1024, pick_words=8) as ctx:
+        assert ctx.placement_for(512 << 10) == sage.SAGE_GLOBAL
+
+
 def test_hybrid_forced_small_region_and_unsupported_geometry(dev):
     """Forced SAGE_HYBRID on an 8 KiB region stages all of it; without its geometry
-    (P = 1, 1024-thread blocks, even block count) it is SAGE_EUNSUPPORTED."""
+    (P = 1 or 4, 1024-thread blocks, even block count) it is SAGE_EUNSUPPORTED."""
     region = make_region(8192)
     d, _keep = to_dev(region, dev)
     with sage.Context(blocks=4, threads=1024, placement=sage.SAGE_HYBRID) as ctx:

@@ -68,6 +68,7 @@ _PROD = re.compile(r"^_ZN4sage20sage_checksum_kernelILi(\d+)ELb(\d)ELb(\d)ELi(\d
 PRODUCT_KERNELS = {
     (1, 1, 0, 16, 18, 4, 0, 2, 7): "c2a: P=1 SMEM, ILP 2 (1 CTA x 1024 threads x 2 lane states per SM)",
     (1, 1, 0, 16, 2, 8, 0, 2, 8): "SAGE_HYBRID (c2c)",
+    (4, 1, 0, 16, 1, 8, 0, 2, 0): "SAGE_HYBRID, P=4 (c2cp4)",
     (1, 1, 0, 16, 32, 4, 0, 1, 0): "P=1 SMEM, ILP 1 (other geometries)",
     (1, 1, 1, 0, 16, 0, 0, 1, 0): "P=1 SMEM, region straddling 4 GiB",
     (1, 0, 1, 16, 16, 0, 0, 1, 0): "P=1 GLOBAL (c3)",
@@ -122,7 +123,7 @@ def test_registers_allow_two_ctas_of_1024(res_usage):
 
 def test_lab_template_matches_the_product_loop():
     """bench/sage_lab.cuh (the experiment harness the timing adversaries are built
-    from) instantiated with the product's c2a and SAGE_HYBRID parameters and every
+    from) instantiated with the product's c2a and SAGE_HYBRID (P = 1, 4) parameters and every
     knob off has the same main-loop instruction stream as the product kernels (up to
     constant-bank offsets and branch addresses), so an adversary kernel is the
     product plus its injection."""
@@ -141,15 +142,18 @@ def test_lab_template_matches_the_product_loop():
                     "0, 7>(const sage_lab::KernelArgs);\n")
             f.write("template __global__ void sage_lab::sage_checksum_kernel<1, true, false, 16, 2, 8, 0, 0, false, 0, 2, "
                     "0, 8>(const sage_lab::KernelArgs);\n")
+            f.write("template __global__ void sage_lab::sage_checksum_kernel<4, true, false, 16, 1, 8, 0, 0, false, 0, 2, "
+                    "0, 0>(const sage_lab::KernelArgs);\n")
         cubin = os.path.join(tmp, "lab_eq.cubin")
         subprocess.run(["nvcc"] + build.ARCH + ["-O3", "-std=c++17", "-cubin", "-o", cubin, cu], check=True,
                        capture_output=True)
         build.build()
         lab = sass_compare.functions(cubin)
         prod = sass_compare.functions(build.CUBIN)
-        for key in ((1, 1, 0, 16, 18, 4, 0, 2, 7), (1, 1, 0, 16, 2, 8, 0, 2, 8)):
+        for key in ((1, 1, 0, 16, 18, 4, 0, 2, 7), (1, 1, 0, 16, 2, 8, 0, 2, 8), (4, 1, 0, 16, 1, 8, 0, 2, 0)):
             pn = [n for n in prod if _product_key(n) == key]
-            ln = [n for n in lab if "ELi%dELi%dELi0ELi0ELb0ELi0ELi2ELi0ELi%dE" % (key[4], key[5], key[8]) in n]
+            ln = [n for n in lab if ("kernelILi%dE" % key[0]) in n and
+                  "ELi%dELi%dELi0ELi0ELb0ELi0ELi2ELi0ELi%dE" % (key[4], key[5], key[8]) in n]
             assert len(pn) == 1 and len(ln) == 1, (pn, ln)
             a = sass_compare.main_loop(cubin, ln[0])
             b = sass_compare.main_loop(build.CUBIN, pn[0])
