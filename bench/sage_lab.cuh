@@ -460,6 +460,31 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
                            "=r"(d.w[4]), "=r"(d.w[5]), "=r"(d.w[6]), "=r"(d.w[7])
                          : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
+    } else if constexpr (SMEM && !STRADDLE && ADDR == 11) {
+        // round 2 (session 2): the P = 1 hybrid with a whole-line L1 prefetch ahead of
+        // each global-side pick (LD 0: prefetch.global.L1 of the pick's 128-B line, then
+        // the load; LD 1: prefetch only the line, load with .L1::evict_last), to test
+        // whether line fills raise the L1 hit rate without costing L1->L2 requests
+        static_assert(P == 1, "ADDR 11 is a P = 1 form");
+        const uint32_t saddr = i * args.four_p + smem_u32(smem_words);
+        const uint64_t gaddr = static_cast<uint64_t>(i) * args.four_p + base;
+        const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
+        const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        if constexpr (LD == 1)
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %1, %2;\n\t"
+                         "@!p prefetch.global.L1 [%4];\n\t"
+                         "@p ld.shared.b32 %0, [%3];\n\t"
+                         "@!p ld.global.nc.L1::evict_last.b32 %0, [%4];\n\t}"
+                         : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        else
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "setp.lt.u32 p, %1, %2;\n\t"
+                         "@!p prefetch.global.L1 [%4];\n\t"
+                         "@p ld.shared.b32 %0, [%3];\n\t"
+                         "@!p ld.global.nc.b32 %0, [%4];\n\t}"
+                         : "=r"(d.w[0]) : "r"(i), "r"(staged_chunks), "r"(saddr), "l"(gaddr));
+        t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 10) {
         // round 2: the ADDR 8 hybrid (FMA-pipe addressing, R6 bracket folded into the
         // chunk-offset IMAD) for P = 4 / 8: LDS.128 x P/4 from the staged prefix, one

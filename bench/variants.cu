@@ -86,6 +86,10 @@ struct V { const char* name; Fn fn; int P; bool smem; bool straddle; int ilp = 1
 #define VARH10(P, U, ILP, ST, PAD) {"P" #P " hybrid10 unroll" #U " ILP" #ILP " stage" #ST " PAD" #PAD, \
                   sage::sage_checksum_kernel<P, true, false, 16, U, 10, 0, 0, false, 0, ILP, 0, PAD>, P, true, false, ILP, 0, ST}
 
+// round 2 (session 2): the P = 1 hybrid with an L1 line prefetch per global pick (ADDR 11, LD 0/1)
+#define VARH11(U, ST, PAD, LD) {"P1 hybrid11 unroll" #U " ILP2 stage" #ST " PAD" #PAD " LD" #LD, \
+                  sage::sage_checksum_kernel<1, true, false, 16, U, 11, LD, 0, false, 0, 2, 0, PAD>, 1, true, false, 2, 0, ST}
+
 #define VARZ(XS, U, A, PAD) {"P1 smem xs" #XS " unroll" #U " addr" #A " ILP2 PAD" #PAD, \
                   sage::sage_checksum_kernel<1, true, false, XS, U, A, 0, 0, false, 0, 2, 0, PAD>, 1, true, false, 2}
 

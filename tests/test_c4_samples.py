@@ -16,7 +16,7 @@ PROFILES = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__
 PATHS = [os.path.join(PROFILES, "r01", f) for f in ("scs2/c4_timing.json", "scs2/c4_timing_full.json",
                                                     "ilp2/c4_timing_full.json", "final/c4_timing_full.json",
                                                     "final/c4_timing_full_v2.json")] + \
-    [os.path.join(PROFILES, "r02", "final", "c4_timing.json")]
+    [os.path.join(PROFILES, "r02", "final", "c4_timing.json"), os.path.join(PROFILES, "r02", "c4", "c4_timing_1000.json")]
 
 
 @pytest.mark.parametrize("path", PATHS)
