@@ -358,12 +358,15 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    region_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     t0 = time.perf_counter()
+    region_ev[0].record(stream)                               # the timed region, on the launching stream
     for k in range(args.warmup, total):
         flush.fill_(k & 0xFF)                                 # L2 flush between timed steps
         ev[k][0].record(stream)
         ctx.attest_async(my_nonces[k], region, R, raw[k])
         ev[k][1].record(stream)
+    region_ev[1].record(stream)
     torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
@@ -371,9 +374,12 @@ def run_ours(args):
     clocks = sampler.stop()
     launches = ctx.launches - launches0
     kern_s = [ev[k][0].elapsed_time(ev[k][1]) / 1e3 for k in range(args.warmup, total)]
-    # the bracket, max over ranks
+    # the bracket: device time of the whole timed region (CUDA events, flushes
+    # included), max over ranks
+    t_dev = region_ev[0].elapsed_time(region_ev[1]) / 1e3
     pdev = dev if backend != "gloo" else None
-    t_bracket = replicas.max_over_ranks(t_wall, pdev)
+    t_bracket = replicas.max_over_ranks(t_dev, pdev)
+    t_wall_max = replicas.max_over_ranks(t_wall, pdev)
     raws = raw.cpu().tolist()
     dec = [sage.decode_raw(r) for r in raws[args.warmup:]]
 
@@ -417,7 +423,7 @@ def run_ours(args):
     mine = {"rank": rank, "device": local, "nonce": "0x%016x" % my_nonces[total - 1],
             "checksum": "0x%016x" % dec[-1].checksum, "cycles": dec[-1].cycles,
             "device_ns": dec[-1].device_ns, "kernel_ms_mean": 1e3 * statistics.mean(kern_s),
-            "kernel_ms_max": 1e3 * max(kern_s), "wall_s": t_wall, "clocks": clocks,
+            "kernel_ms_max": 1e3 * max(kern_s), "wall_s": t_wall, "device_s": t_dev, "clocks": clocks,
             "sampled_parity_sum_ok": (sum(parts) & (2**64 - 1)) == dbg.checksum}
     allr = replicas.gather_results(mine)
 
@@ -437,6 +443,9 @@ def run_ours(args):
                            "parallelism": "independent replica per GPU x%d" % ws,
                            "plumbing": backend or "none",
                            "l2": "256 MiB buffer written between timed steps (flush)"},
+                "timing": {"value": "CUDA events on the launching stream around the K timed steps (L2 flushes "
+                                     "included), max over ranks",
+                           "device_s": t_bracket, "host_wall_s": t_wall_max},
                 "checksummed_gbps": value * 4 * P / 1e9,
                 "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(kern_s), "max": 1e3 * max(kern_s)},
                 "attest_ms": attest_stats(att, verifier),

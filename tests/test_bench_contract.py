@@ -50,6 +50,11 @@ def test_our_arm_one_gpu():
     line = _run(["--config", "c2a", "--rounds", "2000", "--steps", "4", "--warmup", "3"], 900)
     _check_base(line, 1, 4, 3)
     assert line["gpu_launches"] == 4                 # one checksum kernel per timed step
+    # value from the device time of the timed region (CUDA events, max over ranks), which
+    # contains the four kernels and lies inside the host's wall-clock bracket
+    tm = line["timing"]
+    assert abs(line["ms_per_step"] * 4 / 1e3 - tm["device_s"]) < 1e-9
+    assert 4 * line["kernel_ms"]["min"] / 1e3 <= tm["device_s"] <= tm["host_wall_s"]
     rf = line["roofline"]
     assert rf["bound"] == "alu" and 0 < rf["frac"] <= 1 and rf["peak"] > 0
     assert abs(rf["achieved"] / rf["peak"] - rf["frac"]) < 1e-9
