@@ -16,10 +16,17 @@ Two verifier rules, calibrated on honest runs:
     P:313-314; calibrate_session / verify_session on the session median): rejects
     every session of every code-injection adversary, the fastest included, and
     accepts the honest sessions;
-  * per session on the 14th of 16 run times (q = 13/15): the same, and it also
-    rejects sessions in which the fastest adversary cheats in only 5 of the 16
-    challenges (composed from its measured runs and honest ones), which the median
-    lets through by design.
+  * per session on the 14th of 16 run times (q = 13/15): rejects every session of
+    every code-injection adversary.  Its use against partial cheating (the fastest
+    adversary in only 5 of the 16 challenges, composed from its measured runs and
+    honest ones; the median lets that through by design) sits at the noise limit:
+    the cheater's +0.07-0.09% is the size of the honest main mode's drift within
+    one test (the 14th of 16 honest runs reached +0.066% on one box), so the
+    rule's honest acceptance and its partial-cheating rejection trade against each
+    other (92-100% / 95-100% over the test runs).  Both are
+    recorded; with 24 held-out sessions a 4% false-positive rate alone fails a
+    ">= 95% accepted" check one time in four, so they are bounded loosely here
+    (>= 75%) and the gate is the median rule.
 The memory-copy adversary (SMEM placement staged from a clean copy) is measured
 and reported, not asserted: staging reads the region once per CTA, so that attack
 costs nothing per round (DESIGN.md sections 9 and 11)."""
@@ -141,8 +148,9 @@ def test_timing_verifier_rejects_adversaries(adv):
                           if k == "adversaries" else v) for k, v in summary.items() if k != "honest_times_s"}))
     assert summary["honest_restart_frac"] <= 0.05, summary
     assert summary["honest_sessions_accepted_frac"] >= 0.95, summary
-    assert summary["honest_q_sessions_accepted_frac"] >= 0.95, summary
-    assert summary["partial_cheating_5_of_16"]["q_rule_rejected_frac"] >= 0.95, summary["partial_cheating_5_of_16"]
+    # the 14th-of-16 rule at the noise limit (docstring): recorded, loosely bounded
+    assert summary["honest_q_sessions_accepted_frac"] >= 0.75, summary
+    assert summary["partial_cheating_5_of_16"]["q_rule_rejected_frac"] >= 0.75, summary["partial_cheating_5_of_16"]
     for k, name, memcopy in kinds:
         if memcopy:
             continue
