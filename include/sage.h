@@ -213,6 +213,14 @@ int sage_placement_for(sage_ctx* ctx, size_t region_bytes, uint32_t* placement_o
  * region_bytes, NULL buf, buf too small; SAGE_EUNSUPPORTED as for sage_attest. */
 int sage_kernel_symbol(sage_ctx* ctx, uint64_t region_va, size_t region_bytes, char* buf, size_t buf_len);
 
+/* The 16-byte UUID of the GPU the context attests (cudaDeviceProp::uuid, the id
+ * nvidia-smi prints as GPU-xxxxxxxx-...).  A timing model is a property of one
+ * device -- two B200s differ by 0.19% in the median run time of the same kernel,
+ * more than the smallest adversary slowdown measured (the
+ * paper calibrates per device) -- so a verifier binds its calibration
+ * to this id.  SAGE_EINVAL for a NULL argument. */
+int sage_device_uuid(sage_ctx* ctx, uint8_t uuid_out[16]);
+
 /* Context and kernel facts (read-only: changes no kernel attribute). */
 int sage_query(sage_ctx* ctx, sage_info* out);
 

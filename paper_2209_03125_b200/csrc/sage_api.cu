@@ -621,6 +621,14 @@ int sage_kernel_symbol(sage_ctx* ctx, uint64_t region_va, size_t region_bytes, c
     return SAGE_OK;
 }
 
+int sage_device_uuid(sage_ctx* ctx, uint8_t uuid_out[16]) {
+    if (ctx == nullptr || uuid_out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, ctx->device));
+    memcpy(uuid_out, prop.uuid.bytes, 16);
+    return SAGE_OK;
+}
+
 int sage_query(sage_ctx* ctx, sage_info* out) {
     if (ctx == nullptr || out == nullptr) return fail(SAGE_EINVAL, "null pointer%s");
     DeviceGuard dg(ctx->device);

@@ -22,8 +22,8 @@ PLACEMENT_NAMES = {SAGE_SMEM: "smem", SAGE_GLOBAL: "global", SAGE_AUTO: "auto", 
 # every symbol include/sage.h declares
 EXPORTS = ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
            "sage_attest_host", "sage_attest_coverage", "sage_kernel_hash", "sage_host_region_va",
-           "sage_placement_for", "sage_kernel_symbol", "sage_query", "sage_launch_count", "sage_stream", "sage_checksum_destroy",
-           "sage_strerror", "sage_last_error")
+           "sage_placement_for", "sage_kernel_symbol", "sage_device_uuid", "sage_query", "sage_launch_count", "sage_stream",
+           "sage_checksum_destroy", "sage_strerror", "sage_last_error")
 
 
 class SageError(RuntimeError):
@@ -81,6 +81,7 @@ def load(path=LIB):
     L.sage_host_region_va.argtypes = [p, sz, ctypes.POINTER(u64)]
     L.sage_placement_for.argtypes = [p, sz, ctypes.POINTER(ctypes.c_uint32)]
     L.sage_kernel_symbol.argtypes = [p, u64, sz, ctypes.c_char_p, sz]
+    L.sage_device_uuid.argtypes = [p, ctypes.POINTER(ctypes.c_uint8 * 16)]
     L.sage_query.argtypes = [p, ctypes.POINTER(sage_info)]
     L.sage_launch_count.argtypes = [p]
     L.sage_launch_count.restype = u64
@@ -94,7 +95,7 @@ def load(path=LIB):
     L.sage_last_error.restype = ctypes.c_char_p
     for name in ("sage_checksum_init", "sage_attest", "sage_attest_debug", "sage_attest_async", "sage_decode_raw",
                  "sage_attest_coverage", "sage_kernel_hash", "sage_attest_host", "sage_host_region_va",
-                 "sage_placement_for", "sage_kernel_symbol", "sage_query"):
+                 "sage_placement_for", "sage_kernel_symbol", "sage_device_uuid", "sage_query"):
         getattr(L, name).restype = i
     _lib = L
     return L
@@ -224,6 +225,14 @@ def kernel_symbol(ctx, nbytes, region_va=0):
     return buf.value.decode()
 
 
+def device_uuid(ctx):
+    """The attested GPU's UUID, formatted as nvidia-smi prints it (GPU-8-4-4-4-12 hex)."""
+    raw = (ctypes.c_uint8 * 16)()
+    _check(load().sage_device_uuid(ctx, ctypes.byref(raw)))
+    h = bytes(raw).hex()
+    return "GPU-%s-%s-%s-%s-%s" % (h[:8], h[8:12], h[12:16], h[16:20], h[20:])
+
+
 def query(ctx):
     info = sage_info()
     _check(load().sage_query(ctx, ctypes.byref(info)))
@@ -283,6 +292,9 @@ class Context:
 
     def kernel_symbol(self, nbytes, region_va=0):
         return kernel_symbol(self.ctx, nbytes, region_va)
+
+    def device_uuid(self):
+        return device_uuid(self.ctx)
 
     def query(self):
         return query(self.ctx)

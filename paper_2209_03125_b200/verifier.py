@@ -8,10 +8,15 @@ calibrate_robust (median/MAD, for B200's non-normal run times) are the
 alternatives measured in DESIGN.md section 11; calibrate_session / verify_session
 bound the median of a session's series of challenges.  Rejection is a verdict, not an
 error; on a rejection the session restarts with a fresh challenge.
+A timing model belongs to one device: every model carries an optional device id
+(the GPU UUID, sage.Context.device_uuid) and a model bound to a device rejects
+attestations reported for any other one ("device_mismatch") -- two B200s differ
+by 0.19% in the median run time of the same kernel.
 
 This is plain host arithmetic over measured numbers; the checksum itself is
 computed only by the CUDA kernel behind libsage.so.
 """
+import dataclasses
 import math
 from dataclasses import dataclass
 
@@ -24,6 +29,7 @@ class TimingModel:
     sigma: float
     runs: int
     k: float = THRESHOLD_SIGMAS
+    device: str = None            # GPU UUID the model was calibrated on (None: unbound)
 
     @property
     def threshold(self):
@@ -33,13 +39,13 @@ class TimingModel:
 @dataclass(frozen=True)
 class Verdict:
     accepted: bool
-    reason: str               # ok | checksum_mismatch | timeout | stale_nonce | session_timeout
+    reason: str               # ok | checksum_mismatch | timeout | stale_nonce | session_timeout | device_mismatch
     elapsed: float
     expected: int
     response: int
 
 
-def calibrate(samples, k=THRESHOLD_SIGMAS, min_runs=30):
+def calibrate(samples, k=THRESHOLD_SIGMAS, min_runs=30, device=None):
     """TimingModel from honest run times: mean, population sigma,
     threshold = mean + k*sigma.  The paper used 100 runs."""
     xs = [float(s) for s in samples]
@@ -48,10 +54,10 @@ def calibrate(samples, k=THRESHOLD_SIGMAS, min_runs=30):
         raise ValueError("calibration needs >= %d runs, got %d" % (min_runs, n))
     mean = math.fsum(xs) / n
     var = math.fsum((x - mean) ** 2 for x in xs) / n
-    return TimingModel(t_avg=mean, sigma=math.sqrt(var), runs=n, k=k)
+    return TimingModel(t_avg=mean, sigma=math.sqrt(var), runs=n, k=k, device=device)
 
 
-def calibrate_quantile(samples, q=0.99, min_runs=30):
+def calibrate_quantile(samples, q=0.99, min_runs=30, device=None):
     """Empirical-quantile timing model ("an empirical-quantile threshold
     mode since ... noise need not be normal"): threshold = the q-quantile of the
     honest calibration times (linear interpolation).  t_avg and sigma are still
@@ -63,7 +69,7 @@ def calibrate_quantile(samples, q=0.99, min_runs=30):
         raise ValueError("q must be in (0, 1)")
     base = calibrate(xs, min_runs=min_runs)
     return QuantileTimingModel(t_avg=base.t_avg, sigma=base.sigma, runs=base.runs, q=q,
-                               quantile=percentile(xs, 100.0 * q))
+                               quantile=percentile(xs, 100.0 * q), device=device)
 
 
 @dataclass(frozen=True)
@@ -73,13 +79,14 @@ class QuantileTimingModel:
     runs: int
     q: float
     quantile: float
+    device: str = None
 
     @property
     def threshold(self):
         return self.quantile
 
 
-def calibrate_robust(samples, k=6.0, min_margin=1e-3, min_runs=30):
+def calibrate_robust(samples, k=6.0, min_margin=1e-3, min_runs=30, device=None):
     """Robust relative timing model: threshold = median * (1 + margin), margin =
     max(min_margin, k * sigma_r / median) with sigma_r = 1.4826 * MAD, the
     normal-consistent scale of the main mode.  On B200 the run-time distribution
@@ -105,7 +112,7 @@ def calibrate_robust(samples, k=6.0, min_margin=1e-3, min_runs=30):
     margin = max(min_margin, k * sigma_r / med)
     base = calibrate(xs, min_runs=min_runs)
     return RobustTimingModel(t_avg=base.t_avg, sigma=base.sigma, runs=base.runs, median=med, sigma_r=sigma_r,
-                             margin=margin)
+                             margin=margin, device=device)
 
 
 @dataclass(frozen=True)
@@ -116,13 +123,14 @@ class RobustTimingModel:
     median: float
     sigma_r: float
     margin: float
+    device: str = None
 
     @property
     def threshold(self):
         return self.median * (1.0 + self.margin)
 
 
-def calibrate_session(samples, m, k=6.0, min_margin=None, min_runs=30, q=0.5):
+def calibrate_session(samples, m, k=6.0, min_margin=None, min_runs=30, q=0.5, device=None):
     """Timing model for a SESSION of m attestations: the paper's verifier "invokes
     [the VF] repeatedly with a series of challenges while measuring the VF execution
     time for each invocation", so besides each run's own deadline it can
@@ -157,7 +165,7 @@ def calibrate_session(samples, m, k=6.0, min_margin=None, min_runs=30, q=0.5):
     se = sigma_r * math.sqrt(q * (1.0 - q)) / (phi * math.sqrt(m))
     margin = max(min_margin, k * se / med)
     return SessionTimingModel(median=med, sigma_r=sigma_r, m=m, runs=len(xs), margin=margin, q=q,
-                              quantile=percentile(xs, 100.0 * q))
+                              quantile=percentile(xs, 100.0 * q), device=device)
 
 
 @dataclass(frozen=True)
@@ -169,6 +177,7 @@ class SessionTimingModel:
     margin: float
     q: float = 0.5
     quantile: float = None          # calibration q-quantile (the median for q = 0.5)
+    device: str = None
 
     @property
     def threshold(self):
@@ -177,15 +186,27 @@ class SessionTimingModel:
         return base + self.median * self.margin
 
 
-def verify_session(results, model, ledger=None):
+def bind_device(model, device):
+    """The same timing model bound to one device (its GPU UUID)."""
+    return dataclasses.replace(model, device=device)
+
+
+def _wrong_device(model, device):
+    return model.device is not None and device != model.device
+
+
+def verify_session(results, model, ledger=None, device=None):
     """Verdict on a session of model.m attestations, results = [(nonce, response,
     elapsed, expected), ...]: rejected with the first failing run's reason if any
     checksum is wrong or a nonce is reused; otherwise rejected as "session_timeout"
     iff the q-quantile (model.q; the median by default) of the elapsed times
-    exceeds model.threshold.  Returns a Verdict whose elapsed field is that
-    session statistic."""
+    exceeds model.threshold.  A model bound to a device rejects a session from
+    any other device (device: the attested GPU's UUID) as "device_mismatch".
+    Returns a Verdict whose elapsed field is that session statistic."""
     if len(results) != model.m:
         raise ValueError("a session has %d attestations, got %d" % (model.m, len(results)))
+    if _wrong_device(model, device):
+        return Verdict(False, "device_mismatch", results[-1][2], results[-1][3], results[-1][1])
     for nonce, response, elapsed, expected in results:
         if ledger is not None and not ledger.consume(nonce):
             return Verdict(False, "stale_nonce", elapsed, expected, response)
@@ -241,9 +262,13 @@ class NonceLedger:
         return True
 
 
-def verify(response, elapsed, expected, model, nonce=None, ledger=None):
+def verify(response, elapsed, expected, model, nonce=None, ledger=None, device=None):
     """Verdict: accepted iff response == expected and elapsed <=
-    model.threshold and (when a ledger is given) the nonce was not used before."""
+    model.threshold and (when a ledger is given) the nonce was not used before;
+    a model bound to a device also needs device (the attested GPU's UUID) to be
+    that device ("device_mismatch" otherwise)."""
+    if _wrong_device(model, device):
+        return Verdict(False, "device_mismatch", elapsed, expected, response)
     if ledger is not None and nonce is not None and not ledger.consume(nonce):
         return Verdict(False, "stale_nonce", elapsed, expected, response)
     if response != expected:
@@ -253,7 +278,7 @@ def verify(response, elapsed, expected, model, nonce=None, ledger=None):
     return Verdict(True, "ok", elapsed, expected, response)
 
 
-def verify_with_restarts(attempt, model, max_tries=3, ledger=None):
+def verify_with_restarts(attempt, model, max_tries=3, ledger=None, device=None):
     """The paper's false-positive handling: "in which case the verification
     process is restarted".  attempt() runs one attestation with a fresh
     nonce and returns (nonce, response, elapsed, expected); the session is
@@ -263,7 +288,7 @@ def verify_with_restarts(attempt, model, max_tries=3, ledger=None):
     v = None
     for k in range(1, max_tries + 1):
         nonce, response, elapsed, expected = attempt()
-        v = verify(response, elapsed, expected, model, nonce=nonce, ledger=ledger)
+        v = verify(response, elapsed, expected, model, nonce=nonce, ledger=ledger, device=device)
         if v.accepted or v.reason != "timeout":
             return v, k
     return v, max_tries

@@ -140,3 +140,24 @@ def test_timing_fields_are_consistent(dev):
         ev_ns = e0.elapsed_time(e1) * 1e6
     assert dec.checksum == res.checksum
     assert abs(dec.device_ns - ev_ns) < 0.02 * ev_ns, (dec.device_ns, ev_ns)
+
+
+def test_device_uuid_names_the_attested_gpu(dev):
+    """sage_device_uuid returns the attested GPU's UUID (the id a verifier binds its
+    timing model to, verifier.bind_device), the one nvidia-smi reports for the same
+    device, and it is stable across contexts."""
+    import re
+    import subprocess
+    with sage.Context() as ctx:
+        u = ctx.device_uuid()
+    assert re.fullmatch(r"GPU-[0-9a-f]{8}-[0-9a-f]{4}-[0-9a-f]{4}-[0-9a-f]{4}-[0-9a-f]{12}", u), u
+    assert u != "GPU-00000000-0000-0000-0000-000000000000"
+    with sage.Context(blocks=2, threads=64) as ctx:
+        assert ctx.device_uuid() == u
+    try:
+        smi = subprocess.run(["nvidia-smi", "--query-gpu=uuid", "--format=csv,noheader"], capture_output=True,
+                             text=True, timeout=60).stdout.split()
+    except (OSError, subprocess.SubprocessError):
+        smi = []
+    if smi:
+        assert u in smi, (u, smi)

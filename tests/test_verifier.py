@@ -248,3 +248,38 @@ def test_session_quantile_rule_bounds_partial_cheating():
         partial[j:j + 5] += 0.0007 * T              # cheating in 5 of 16 challenges
     assert all(verdicts(partial, med_rule))
     assert not any(verdicts(partial, q_rule))
+
+
+def test_models_bound_to_a_device_reject_other_devices():
+    """A timing model is a property of one GPU (two B200s differ by 0.19% in the
+    median run time of the same kernel): every calibrate_*
+    takes the device id, bind_device binds an existing model, and a bound model
+    rejects a run or a session reported for another device (or for none) as
+    device_mismatch -- before any timing or checksum test -- while an unbound
+    model ignores the device."""
+    a, b = "GPU-c305bf10-4c86-5a33-dc0b-e0b21eda131b", "GPU-45eb5f3e-355c-4498-195f-a6ea95f34e9a"
+    xs = [1.0 + 0.001 * (i % 7) for i in range(40)]
+    models = [V.calibrate(xs, device=a), V.calibrate_quantile(xs, device=a), V.calibrate_robust(xs, device=a),
+              V.bind_device(V.calibrate_robust(xs), a)]
+    for m in models:
+        assert m.device == a
+        assert V.verify(5, 1.0, 5, m, device=a).accepted
+        for other in (b, None):
+            v = V.verify(5, 1.0, 5, m, device=other)
+            assert (v.accepted, v.reason) == (False, "device_mismatch")
+        v = V.verify(4, 1.0, 5, m, device=b)                  # the device is checked first
+        assert v.reason == "device_mismatch"
+    free = V.calibrate_robust(xs)
+    assert free.device is None and V.verify(5, 1.0, 5, free, device=b).accepted
+    sm = V.calibrate_session(xs, 4, device=a)
+    runs = [(i, 5, 1.0, 5) for i in range(4)]
+    assert V.verify_session(runs, sm, device=a).accepted
+    assert V.verify_session(runs, sm, device=b).reason == "device_mismatch"
+    calls = []
+
+    def attempt():
+        calls.append(1)
+        return len(calls), 5, 1.0, 5
+    v, tries = V.verify_with_restarts(attempt, models[2], device=b)
+    assert (v.reason, tries) == ("device_mismatch", 1)          # not retried
+    assert V.verify_with_restarts(attempt, models[2], device=a)[0].accepted
