@@ -167,9 +167,56 @@ int gather_only(size_t mb, int op) {
     return 0;
 }
 
+// Concurrency sweep of the dependent random-sector gather (round 2, session 2):
+// the same MLP-1 probe over a power-of-two buffer with 1 .. 2048 chains per SM
+// (blocks = SMs or 2 x SMs, 32 .. 1024 threads).  Little's law gives the mean
+// latency per pick, concurrency / rate: a rate that stops growing while the
+// latency grows with the concurrency is a throughput limit in the memory system
+// (queueing), not a latency limit.
+int gather_concurrency(size_t mb) {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    Args a{};
+    a.c3 = 7;
+    CK(cudaMalloc(&a.sink, 4));
+    size_t bytes = mb << 20;
+    if (bytes & (bytes - 1)) { fprintf(stderr, "power-of-two MiB only\n"); return 1; }
+    uint32_t* buf = nullptr;
+    CK(cudaMalloc(&buf, bytes));
+    CK(cudaMemset(buf, 1, bytes));
+    const uint32_t mask = uint32_t(bytes / 32 - 1);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int shapes[][2] = {{1, 32}, {1, 64}, {1, 128}, {1, 256}, {1, 512}, {1, 1024}, {2, 1024}};
+    for (auto& sh : shapes) {
+        const int blocks = sh[0] * sms, threads = sh[1];
+        a.iters = threads >= 512 ? 2048 : 4096;
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            CK(cudaEventRecord(e0));
+            p_hbm_gather_mlp<1, 0><<<blocks, threads>>>(a, buf, mask);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaGetLastError());
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            if (ms < best) best = ms;
+        }
+        const double conc = double(blocks) * threads, picks = conc * a.iters, rate = picks / (best * 1e-3);
+        printf("{\"probe\": \"hbm_gather_concurrency\", \"mib\": %zu, \"chains_per_sm\": %d, \"concurrency\": %.0f, "
+               "\"picks_per_s\": %.4e, \"little_latency_ns\": %.1f, \"ms\": %.3f}\n",
+               mb, blocks / sms * threads, conc, rate, 1e9 * conc / rate, best);
+        fflush(stdout);
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
     if (argc > 2 && strcmp(argv[1], "gather") == 0)
         return gather_only(strtoull(argv[2], nullptr, 10), argc > 3 ? atoi(argv[3]) : 0);
+    if (argc > 2 && strcmp(argv[1], "conc") == 0)
+        return gather_concurrency(strtoull(argv[2], nullptr, 10));
     int dev = 0, sms = 0, clk = 0;
     CK(cudaSetDevice(dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
