@@ -63,7 +63,7 @@ extern "C" {
 /* region placement */
 #define SAGE_AUTO   0u  /* SMEM up to smem_region_max (64 KiB, or 128 KiB at the ILP-2 geometry:
                            P = 1, 1024-thread blocks, even block count); then HYBRID up to
-                           1 MiB at that geometry (P = 4: HYBRID from 512 KiB to 1 MiB at
+                           1 MiB at that geometry (P = 4: HYBRID from 256 KiB to 1 MiB at
                            the same block geometry); else GLOBAL (always for P = 8) */
 #define SAGE_SMEM   1u  /* region staged once per CTA into shared memory (TMA bulk copy) */
 #define SAGE_GLOBAL 2u  /* region read in place from L2/HBM every round */
@@ -72,7 +72,7 @@ extern "C" {
                            or 4, 1024-thread blocks, an even block count and a region whose chunk
                            addresses share their high 32 bits (one CTA x 1024 threads x 2
                            lane states per SM); SAGE_AUTO picks it for 128 KiB < region <=
-                           1 MiB (P = 1) or 512 KiB <= region <= 1 MiB (P = 4) when those
+                           1 MiB (P = 1) or 256 KiB <= region <= 1 MiB (P = 4) when those
                            hold */
 
 typedef struct sage_ctx sage_ctx;

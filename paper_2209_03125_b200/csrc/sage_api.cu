@@ -54,12 +54,12 @@ constexpr size_t kSmemRegionMaxIlp2 = 128 * 1024;
 // <= 1 MiB: 61.7 / 75.6 / 18.1 ms (R = 2e4) vs 64.0 / 93.7 / 18.8 ms GLOBAL at
 // 256 KiB / 512 KiB / 1 MiB.
 constexpr size_t kHybridStage = 192 * 1024, kHybridRegionMax = 1024 * 1024;
-// P = 4 (16-B picks) takes SAGE_HYBRID from 512 KiB: 75.8 vs 89.1 ms GLOBAL at the
-// paper's 524,288-B buffer (R = 1e5), 17.5-18.4 vs 18.9 ms at 1 MiB (R = 2e4); at
-// 256 KiB the fully-read-in-place form is faster (65.6-72.5 vs 69.4 ms),
-// profiles/r02/c2c48/.  P = 8 stays GLOBAL: its staged picks (two LDS.128 each) are
-// slower than L1 (117.3 vs 113.8 ms at 512 KiB).
-constexpr size_t kHybridRegionMinP4 = 512 * 1024;
+// P = 4 (16-B picks) takes SAGE_HYBRID from 256 KiB: 69.5 vs 72.6 ms GLOBAL at
+// 256 KiB, 75.9 vs 89.9 ms at the paper's 524,288-B buffer (R = 1e5), 18.3 vs
+// 18.9 ms at 1 MiB (R = 2e4); at 128 KiB GLOBAL is faster (65.1 vs 66.3 ms)
+// (profiles/r02/c2c48/p4_tiers.jsonl).  P = 8 stays GLOBAL: its staged picks (two
+// LDS.128 each) are slower than L1 (117.3 vs 113.8 ms at 512 KiB).
+constexpr size_t kHybridRegionMinP4 = 256 * 1024;
 
 using KernelFn = void (*)(const sage::KernelArgs);
 

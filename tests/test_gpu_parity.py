@@ -468,13 +468,13 @@ def test_hybrid_placement_bit_exact(dev, nbytes):
     assert out[sage.SAGE_AUTO].checksum == out[sage.SAGE_GLOBAL].checksum == want
 
 
-@pytest.mark.parametrize("nbytes,auto", [(256 << 10, sage.SAGE_GLOBAL), (512 << 10, sage.SAGE_HYBRID),
-                                         (1 << 20, sage.SAGE_HYBRID)])
+@pytest.mark.parametrize("nbytes,auto", [(128 << 10, sage.SAGE_GLOBAL), (256 << 10, sage.SAGE_HYBRID),
+                                         (512 << 10, sage.SAGE_HYBRID), (1 << 20, sage.SAGE_HYBRID)])
 def test_hybrid_p4_bit_exact(dev, nbytes, auto):
     """The P = 4 SAGE_HYBRID form (16-B picks; LDS.128 from the staged 192 KiB,
-    LDG.128 in place): SAGE_AUTO takes it from 512 KiB to 1 MiB (GLOBAL below, where
-    reading in place is faster); forced, auto and GLOBAL placements are bit-exact with
-    the oracle."""
+    LDG.128 in place): SAGE_AUTO takes it from 256 KiB to 1 MiB (GLOBAL at 128 KiB,
+    where reading in place is faster); forced, auto and GLOBAL placements are
+    bit-exact with the oracle."""
     region = make_region(nbytes, prefix=launched_kernel_prefix(nbytes, blocks=2, threads=1024, pick_words=4),
                          fill_seed=nbytes + 4)
     d, _keep = to_dev(region, dev, align_offset=16)
