@@ -77,6 +77,46 @@ def test_random_small_geometries(dev, seed):
         assert parts[w] == oracle.warp_sum(nonce, region, d.data_ptr(), rounds, w, P)
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_random_ilp2_geometries(dev, seed):
+    """Random cases at the ILP-2 geometry (1024-thread blocks, even block count: the
+    c2a SMEM kernel and the P = 1 / 4 SAGE_HYBRID kernels): random P in {1, 4},
+    region size (16 B ... 1 MiB; HYBRID stages min(region, 192 KiB)), placement
+    (AUTO, SMEM where it fits, HYBRID, GLOBAL), rounds (0 ... 300, covering the
+    unrolled trips and remainders), nonce and alignment; bit-exact with the oracle,
+    one sampled warp partial each."""
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(6):
+        P = int(rng.choice([1, 4]))
+        nbytes = 1 << int(rng.integers(4, 21))
+        nc = nbytes // (4 * P)
+        if nc < 1:
+            continue
+        choices = [sage.SAGE_AUTO, sage.SAGE_HYBRID, sage.SAGE_GLOBAL]
+        if nbytes <= (128 << 10 if P == 1 else 64 << 10):
+            choices.append(sage.SAGE_SMEM)
+        placement = int(rng.choice(choices))
+        blocks = 2 * int(rng.integers(1, 3))
+        rounds = int(rng.integers(0, 300))
+        nonce = int(rng.integers(0, 2**64, dtype=np.uint64))
+        region = make_region(nbytes, fill_seed=int(rng.integers(0, 2**31)))
+        d, _keep = to_dev(region, dev, align_offset=32 * int(rng.integers(0, 8)))
+        if (d.data_ptr() >> 32) != ((d.data_ptr() + nbytes - 1) >> 32):
+            placement = sage.SAGE_AUTO            # the ILP-2 forms need one 4 GiB window
+        pw = torch.zeros(blocks * 1024 // 32, dtype=torch.int64, device=dev)
+        with sage.Context(blocks=blocks, threads=1024, pick_words=P, placement=placement) as ctx:
+            res = ctx.attest_debug(nonce, d, rounds, pw)
+        want = oracle.attest(nonce, region, d.data_ptr(), rounds, blocks, 1024, P)
+        case = dict(P=P, nbytes=nbytes, placement=placement, used=res.placement, ilp=res.ilp, blocks=blocks,
+                    rounds=rounds)
+        assert res.checksum == want, case
+        if placement == sage.SAGE_HYBRID or (placement == sage.SAGE_SMEM and P == 1):
+            assert res.ilp == 2, case
+        parts = [int(v) & M64 for v in pw.cpu().tolist()]
+        w = int(rng.integers(0, len(parts)))
+        assert parts[w] == oracle.warp_sum(nonce, region, d.data_ptr(), rounds, w, P), case
+
+
 def test_tiny_regions_below_bulk_granule(dev):
     """Nc = 1 and 2 with P = 1 (4- and 8-byte regions) take the non-TMA staging path."""
     for nbytes in (4, 8):
