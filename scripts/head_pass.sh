@@ -1,4 +1,4 @@
-O=gpurun_out/r2s2_head
+O=${O:-gpurun_out/r2s2_head}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv > $O/smi_start.csv
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1

@@ -42,7 +42,7 @@ import oracle                                                     # noqa: E402
 from paper_2209_03125_b200 import sage, verifier                  # noqa: E402
 from paper_2209_03125_b200.inputs import launched_kernel_prefix, make_region, nonces  # noqa: E402
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.statistical]
 R = 100_000
 PASSES, HONEST_PER_PASS, CALIB, SESSION = 96, 5, 96, 16
 FASTEST = "+1 IMAD / round (attacker-searched schedule)"     # within single-run noise
