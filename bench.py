@@ -95,7 +95,36 @@ def random_gather_ceiling(region_bytes):
         return None
 
 
-def roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, workload, gather_ceiling=None):
+# Bytes of the region SAGE_HYBRID stages in shared memory (sage_api.cu kHybridStage);
+# the rest of its picks go through L1 to L2.
+HYBRID_STAGE = 192 * 1024
+
+
+def l2_request_ceiling(placement, region_bytes):
+    """L0 probe (bench/microbench.cu l2gather) for an L2-resident region read in
+    place (GLOBAL <= 1 MiB, or SAGE_HYBRID's part above the staged prefix):
+    dependent random 4-B reads, one per 32-B sector of that window, in the hybrid
+    kernel's geometry -- the measured ceiling of the L1->L2 request path for the
+    pick pattern without any checksum arithmetic.  Returns (picks/s, fraction of
+    the kernel's picks that take that path) or None."""
+    if region_bytes > (1 << 20) or placement not in ("hybrid", "global"):
+        return None
+    skip = min(HYBRID_STAGE, region_bytes) if placement == "hybrid" else 0
+    if skip >= region_bytes:
+        return None
+    exe = os.path.join(ROOT, "bench", "microbench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "l2gather", str(region_bytes), str(skip)], capture_output=True, text=True,
+                             timeout=120).stdout
+        return json.loads(out.strip().splitlines()[-1])["picks_per_s"], (region_bytes - skip) / region_bytes
+    except (subprocess.SubprocessError, ValueError, IndexError, KeyError):
+        return None
+
+
+def roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, workload, gather_ceiling=None,
+             l2_ceiling=None):
     """Roofline record of the checksum kernel.  HBM regions
     (GLOBAL, > 1 MiB): one 32-B DRAM sector per pick against hbm_gbs; everything
     else: algorithmic 32-bit integer ops per thread-round against the issue peak."""
@@ -117,10 +146,15 @@ def roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, workload,
           "peak_source": "%d SMs x 4 SMSP x 32 lanes x 1 issue/clk x %s sm_max_mhz %.0f (DESIGN.md 7)"
                          % (sms, peak_src, f_clk / 1e6)}
     if placement == "hybrid":
-        rf["binding_limit"] = ("L1->L2 miss requests, not the ALU: 62.5% of the picks miss the 192 KiB staged "
-                               "prefix (DESIGN.md section 7); frac is the integer-issue fraction")
+        rf["binding_limit"] = ("L1->L2 miss requests, not the ALU: the picks above the 192 KiB staged prefix "
+                               "go through L1 to L2 (DESIGN.md section 7); frac is the integer-issue fraction")
     elif placement == "global":
         rf["binding_limit"] = "L1/L2 pick latency and requests (L2-resident region), DESIGN.md section 7"
+    if l2_ceiling:
+        ceil, share = l2_ceiling
+        rf["l2_request_ceiling_picks_per_s"] = ceil
+        rf["l2_picks_share"] = share
+        rf["frac_of_l2_request_ceiling"] = n * R * share / mean_k / ceil
     return rf
 
 
@@ -253,6 +287,7 @@ def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms):
         n = info.blocks * info.threads
         placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
         ceiling = random_gather_ceiling(nbytes) if nbytes > (1 << 20) else None
+        l2c = l2_request_ceiling(placement, nbytes)
         warm_up(ctx, region, R, nonces, 2, 0, stream, dev, flush)
         raw = torch.zeros(EXTRA_STEPS, 4, dtype=torch.int64, device=dev)
         sampler = ClockSampler(dev.index).start()
@@ -273,7 +308,8 @@ def run_extra(ctx_args, dev, stream, flush, peaks, peak_src, sms):
                      "steps": EXTRA_STEPS, "gpu_launches": ctx.launches - launches0,
                      "kernel_ms": {"mean": 1e3 * mean_k, "min": 1e3 * min(ks), "max": 1e3 * max(ks)},
                      "thread_rounds_per_s": n * R / mean_k, "checksummed_gbps": n * R * 4 * P / mean_k / 1e9,
-                     "roofline": roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, name, ceiling),
+                     "roofline": roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, name, ceiling,
+                                          l2c),
                      "clocks": clocks}
         ctx.close()
         del region
@@ -348,6 +384,7 @@ def run_ours(args):
     info = ctx.query()
     n = info.blocks * info.threads
     placement = sage.PLACEMENT_NAMES[ctx.placement_for(nbytes)]
+    l2_ceiling = l2_request_ceiling(placement, nbytes) if rank == 0 else None
     my_nonces = replicas.replica_nonces(rank, args.warmup + args.steps + 64)
     total = args.warmup + args.steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -453,7 +490,7 @@ def run_ours(args):
         if clocks.get("power_w_median"):
             line["energy_j_per_attestation"] = clocks["power_w_median"] * mean_k
         line["roofline"] = roofline(placement, nbytes, P, n, R, mean_k, peaks, peak_src, sms, args.config,
-                                    gather_ceiling)
+                                    gather_ceiling, l2_ceiling)
         if ws > 1:
             line["replicas"] = allr
         if ws == 1 and not args.no_cpu_baseline:

@@ -167,6 +167,71 @@ int gather_only(size_t mb, int op) {
     return 0;
 }
 
+// Dependent random-sector gather over an L2-resident window (round 2, session 3):
+// the MLP-1 chain of p_hbm_gather_mlp, but each pick is one 4-B load from a
+// random 32-B sector of [skip, skip + span) inside a buffer of `total` bytes
+// (non-power-of-two spans by a multiply-high range reduction).  With
+// total = 524,288 and skip = 192 KiB this is the in-place part of the paper's
+// buffer under SAGE_HYBRID -- every pick an L1 miss to an L2 hit, no checksum
+// arithmetic: the measured ceiling of the L1->L2 request path for that pattern
+// (bench.py's c2c / c2cp4 / c2cp8 roofline records).  Geometry as the hybrid
+// kernel: one CTA x 1024 threads x 2 chains per SM, 192 KiB shared memory reserved.
+template <int OP>
+__global__ void __launch_bounds__(1024, 1) p_l2_gather(Args a, const uint32_t* __restrict__ buf, uint32_t nsect) {
+    // two independent chains per thread, one CTA of 1024 threads per SM: the
+    // SAGE_HYBRID kernel's geometry (two lane states per thread)
+    uint32_t x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 0x9E3779B9u + a.c3, x1 = x0 ^ 0x85EBCA77u;
+    for (uint32_t it = 0; it < a.iters; ++it) {
+        x0 = x0 * 1664525u + 1013904223u;
+        x1 = x1 * 1664525u + 1013904223u;
+        const uint32_t w0 = gather_load<OP>(buf + __umulhi(x0, nsect) * 8u);
+        const uint32_t w1 = gather_load<OP>(buf + __umulhi(x1, nsect) * 8u);
+        x0 ^= w0;
+        x1 ^= w1;
+    }
+    if ((x0 ^ x1) == 0x12345679u) a.sink[0] = x0;
+}
+
+int l2_gather(size_t total, size_t skip, int op) {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    if (skip >= total || total % 32 || skip % 32) { fprintf(stderr, "need 0 <= skip < total, multiples of 32\n"); return 1; }
+    Args a{};
+    a.c3 = 7;
+    CK(cudaMalloc(&a.sink, 4));
+    uint32_t* buf = nullptr;
+    CK(cudaMalloc(&buf, total));
+    CK(cudaMemset(buf, 1, total));
+    const uint32_t nsect = uint32_t((total - skip) / 32);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    a.iters = 16384;   // ~20 ms per launch: long enough for the clocks to settle
+    void (*fns[])(Args, const uint32_t*, uint32_t) = {p_l2_gather<0>, p_l2_gather<1>, p_l2_gather<2>, p_l2_gather<3>};
+    // the same shared-memory carve-out as the hybrid kernel: 192 KiB of dynamic shared
+    // memory per CTA (unused), which leaves L1 the rest of the SM's 256 KB
+    const int dyn = 192 * 1024;
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fns[op & 3]), cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaEventRecord(e0));
+        fns[op & 3]<<<sms, 1024, dyn>>>(a, buf + skip / 4, nsect);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaGetLastError());
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep > 0 && ms < best) best = ms;   // first launch warms L2
+    }
+    const double picks = double(sms) * 1024 * 2 * a.iters;
+    int clk_khz = 0;
+    CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
+    printf("{\"probe\": \"l2_gather\", \"total_bytes\": %zu, \"skip_bytes\": %zu, \"op\": %d, "
+           "\"picks_per_s\": %.4e, \"picks_per_sm_clk_at_max\": %.4f, \"ms\": %.3f}\n",
+           total, skip, op, picks / (best * 1e-3), picks / (best * 1e-3) / sms / (clk_khz * 1e3), best);
+    return 0;
+}
+
 // Concurrency sweep of the dependent random-sector gather (round 2, session 2):
 // the same MLP-1 probe over a power-of-two buffer with 1 .. 2048 chains per SM
 // (blocks = SMs or 2 x SMs, 32 .. 1024 threads).  Little's law gives the mean
@@ -215,6 +280,8 @@ int gather_concurrency(size_t mb) {
 int main(int argc, char** argv) {
     if (argc > 2 && strcmp(argv[1], "gather") == 0)
         return gather_only(strtoull(argv[2], nullptr, 10), argc > 3 ? atoi(argv[3]) : 0);
+    if (argc > 3 && strcmp(argv[1], "l2gather") == 0)
+        return l2_gather(strtoull(argv[2], nullptr, 10), strtoull(argv[3], nullptr, 10), argc > 4 ? atoi(argv[4]) : 0);
     if (argc > 2 && strcmp(argv[1], "conc") == 0)
         return gather_concurrency(strtoull(argv[2], nullptr, 10));
     int dev = 0, sms = 0, clk = 0;

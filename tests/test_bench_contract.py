@@ -87,3 +87,32 @@ def test_our_arm_two_replicas_torchrun():
     assert all({"sm_mhz", "sm_max_mhz", "reasons", "power_w_median"} <= set(r["clocks"]) for r in reps)
     assert all(r["kernel_ms_mean"] > 0 for r in reps)
     assert "cpu_baseline" not in line                 # rank 0 at N=1 only
+
+
+def _bench_module():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_main", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_roofline_records_on_cpu():
+    """The roofline record's arithmetic (no GPU): the integer-issue fraction of an
+    SMEM run, the HBM sector fraction, and the L1->L2 request-ceiling fraction of a
+    SAGE_HYBRID run counts only the picks above the staged prefix."""
+    b = _bench_module()
+    peaks = {"hbm_gbs": 6400.0, "sm_max_mhz": 2000.0}
+    n, R, t = 303104, 100_000, 0.05
+    rf = b.roofline("smem", 8192, 1, n, R, t, peaks, "test", 148, "none")
+    assert rf["bound"] == "alu" and rf["ops_per_thread_round"] == 59
+    assert rf["frac"] == pytest.approx(n * R * 59 / t / (148 * 4 * 32 * 2e9))
+    assert "l2_request_ceiling_picks_per_s" not in rf
+    rf = b.roofline("global", 256 << 20, 1, n, 10_000, t, peaks, "test", 148, "none", gather_ceiling=1e11)
+    assert rf["bound"] == "hbm" and rf["frac"] == pytest.approx(n * 1e4 * 32 / t / 1e9 / 6400.0)
+    assert rf["frac_of_random_gather_ceiling"] == pytest.approx(n * 1e4 / t / 1e11)
+    share = (524288 - b.HYBRID_STAGE) / 524288
+    assert share == 0.625
+    rf = b.roofline("hybrid", 524288, 1, n, R, t, peaks, "test", 148, "none", l2_ceiling=(2.7e11, share))
+    assert rf["frac_of_l2_request_ceiling"] == pytest.approx(n * R * share / t / 2.7e11)
+    assert b.l2_request_ceiling("smem", 8192) is None and b.l2_request_ceiling("global", 256 << 20) is None
