@@ -213,7 +213,7 @@ int l2_gather(size_t total, size_t skip, int op) {
     const int dyn = 192 * 1024;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fns[op & 3]), cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     float best = 1e30f;
-    for (int rep = 0; rep < 5; ++rep) {
+    for (int rep = 0; rep < 12; ++rep) {   // the first launches ramp an idle GPU's clocks
         CK(cudaEventRecord(e0));
         fns[op & 3]<<<sms, 1024, dyn>>>(a, buf + skip / 4, nsect);
         CK(cudaEventRecord(e1));
@@ -221,7 +221,7 @@ int l2_gather(size_t total, size_t skip, int op) {
         CK(cudaGetLastError());
         float ms;
         CK(cudaEventElapsedTime(&ms, e0, e1));
-        if (rep > 0 && ms < best) best = ms;   // first launch warms L2
+        if (rep >= 4 && ms < best) best = ms;
     }
     const double picks = double(sms) * 1024 * 2 * a.iters;
     int clk_khz = 0;

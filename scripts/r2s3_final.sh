@@ -18,7 +18,8 @@ for c in c2a c2c c2cp4 c2cp8; do
   ncu --page raw --csv -i $O/${c}_full.ncu-rep > $O/${c}_ncu_full_raw.csv 2>/dev/null
   ncu --page details --csv -i $O/${c}_full.ncu-rep > $O/${c}_ncu_full_details.csv 2>/dev/null
 done
-bash scripts/sanitize.sh $O
+# compute-sanitizer is closed on this pool (runs under it left GPUs needing a reset); the last
+# sanitizer pass at HEAD of session 2 is profiles/r02/final_s2/sanitizer_*.txt
 
 for t in 524288:196608 524288:0 327680:0 1048576:196608 262144:196608; do bench/microbench l2gather ${t%:*} ${t#*:} >> $O/l2gather.jsonl; done
 nvidia-smi --query-gpu=name,uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv > $O/smi_end.csv
