@@ -11,6 +11,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsage.so")
+# Test-only bounds-checked build of the same sources (-DSAGE_BOUNDS_CHECK: every
+# shared / global address a kernel reads is checked and a violation traps); not
+# the product, kept beside the other test-only library under bench/.
+CHECKED_LIB = os.path.join(ROOT, "bench", "libsage_checked.so")
 CUBIN = os.path.join(PKG, "sage_kernel.cubin")
 SOURCES = [os.path.join(CSRC, "sage_api.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "sage_kernel.cuh"), os.path.join(CSRC, "sage_hash.cuh"),
@@ -63,6 +67,21 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_checked(force=False):
+    """Compile the bounds-checked library (CHECKED_LIB) if stale.  Register spills
+    are allowed here: it is a correctness instrument, not timed."""
+    if force or _stale(CHECKED_LIB):
+        tmp = CHECKED_LIB + ".%d.tmp" % os.getpid()
+        cmd = [_nvcc()] + ARCH + FLAGS + ["-DSAGE_BOUNDS_CHECK", "-shared", "-Xcompiler", "-fPIC", "-o", tmp] + SOURCES
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError("nvcc (bounds-checked build) failed:\n" + p.stdout + p.stderr)
+        os.replace(tmp, CHECKED_LIB)
+    return CHECKED_LIB
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))
     print(LIB)

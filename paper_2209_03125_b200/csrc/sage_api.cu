@@ -7,6 +7,7 @@
 #include <time.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -352,6 +353,11 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     args.per_warp = per_warp;
     args.counts = counts;
     sage::fill_tables(args, c->pick_words);
+#ifdef SAGE_BOUNDS_CHECK
+    // bounds-checked build only: a negative control for the checks -- tell the kernel
+    // one chunk less is staged than its picks can reach, which must trap
+    if (dyn && getenv("SAGE_CHECK_SELFTEST")) args.region_bytes -= 4u * c->pick_words;
+#endif
     fn<<<c->blocks / ilp, c->threads, dyn, c->stream>>>(args);
     cudaError_t le = cudaGetLastError();
     if (le == cudaErrorInvalidValue && dyn) {

@@ -64,6 +64,28 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// ---- bounds-checked build (test-only: bench/libsage_checked.so, -DSAGE_BOUNDS_CHECK) ----
+// Every shared-memory and global address the kernel reads is checked against the
+// staged bytes / the region, and a violation traps (the launch fails with an
+// error instead of reading out of bounds).  The product build compiles these to
+// nothing (tests/test_sass_evidence.py: no trap instruction in libsage.so).
+#ifdef SAGE_BOUNDS_CHECK
+#define SAGE_CHECK(cond)          \
+    do {                          \
+        if (!(cond)) __trap();    \
+    } while (0)
+#else
+#define SAGE_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+    uint32_t r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+
 // ---- PTX helpers: mbarrier + 1-D TMA bulk copy + read-only loads ------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -223,6 +245,10 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
     const uint32_t C = a[kAccum - 1];
     const uint32_t i = (static_cast<uint32_t>(y >> 32) ^ C) & nc_mask;
     if constexpr (COUNT) atomicAdd(&args.counts[i], 1u);
+    // bounds-checked build: the region is (nc_mask + 1) chunks of 4P bytes at base;
+    // shared memory holds its first args.region_bytes bytes
+    const uint64_t region_end = base + (static_cast<uint64_t>(nc_mask) + 1u) * (4u * P);
+    (void)region_end;
     // R4, R5, R6 (first part)
     Pick<P> d;
     uint32_t t;
@@ -230,6 +256,7 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         // as ADDR == 2, with the whole warp-uniform bracket folded into the chunk-offset IMAD
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        SAGE_CHECK(addr - smem_u32(smem_words) + 4u * P <= args.region_bytes);
         d = load_shared_addr<P>(addr);
         t = static_cast<uint32_t>(y) * args.one + (i * args.four_p + ur);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 8) {
@@ -241,6 +268,8 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         const uint64_t gaddr = static_cast<uint64_t>(i) * args.four_p + base;
         const uint32_t staged_chunks = args.region_bytes / args.four_p;   // loop-invariant
         const uint32_t ur = r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH;
+        SAGE_CHECK(i < staged_chunks ? saddr - smem_u32(smem_words) + 4u * P <= args.region_bytes
+                                     : gaddr >= base + args.region_bytes && gaddr + 4u * P <= region_end);
         if constexpr (P == 1) {
             asm volatile("{\n\t.reg .pred p;\n\t"
                          "setp.lt.u32 p, %1, %2;\n\t"
@@ -270,11 +299,13 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         // both chunk offsets and the R6 add as IMADs (FMA pipe), sparing the ALU pipe
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
         const uint32_t lo_dp = i * args.four_p + static_cast<uint32_t>(base);
+        SAGE_CHECK(addr - smem_u32(smem_words) + 4u * P <= args.region_bytes);
         d = load_shared_addr<P>(addr);
         t = static_cast<uint32_t>(y) * args.one + lo_dp + (r * kKR + static_cast<uint32_t>(base >> 32) * kKH);
     } else if constexpr (SMEM && !STRADDLE && ADDR == 1) {
         // shared-window address of the chunk on the FMA pipe; lo32(dp) = addr + (lo32(base) - smem)
         const uint32_t addr = i * args.four_p + smem_u32(smem_words);
+        SAGE_CHECK(addr - smem_u32(smem_words) + 4u * P <= args.region_bytes);
         d = load_shared_addr<P>(addr);
         const uint32_t base_minus_smem = static_cast<uint32_t>(base) - smem_u32(smem_words);   // loop-invariant
         // lo32(y) + r*KR + lo32(dp) + hi32(dp)*KH with lo32(dp) = addr + base_minus_smem; the bracket is
@@ -282,10 +313,13 @@ __device__ __forceinline__ void scs_round(uint32_t (&a)[kAccum], uint32_t& xlo, 
         t = static_cast<uint32_t>(y) + (r * kKR + base_minus_smem + static_cast<uint32_t>(base >> 32) * kKH) + addr;
     } else if constexpr (SMEM && !STRADDLE) {
         const uint32_t v = i * (4u * P);                         // byte offset of the chunk
+        SAGE_CHECK(v + 4u * P <= args.region_bytes);
         d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
         t = static_cast<uint32_t>(y) + (r * kKR + static_cast<uint32_t>(base) + static_cast<uint32_t>(base >> 32) * kKH) + v;
     } else {
         const uint64_t dp = base + static_cast<uint64_t>(i) * (4u * P);   // R5 (= the global load address)
+        SAGE_CHECK(SMEM ? (static_cast<uint64_t>(i) + 1u) * (4u * P) <= args.region_bytes
+                        : dp >= base && dp + 4u * P <= region_end);
         if constexpr (SMEM) d = load_shared<P>(smem_words + static_cast<size_t>(i) * P);
         else d = load_global<P>(reinterpret_cast<const uint32_t*>(dp));
         t = static_cast<uint32_t>(y) + r * kKR + static_cast<uint32_t>(dp) + static_cast<uint32_t>(dp >> 32) * kKH;
@@ -333,6 +367,8 @@ __global__ void __launch_bounds__(1024, ILP == 1 ? 2 : 1) sage_checksum_kernel(c
     // a2: stage the region (or its prefix, HYBRID) into shared memory.
     if constexpr (SMEM) {
         const uint32_t bytes = args.region_bytes;
+        SAGE_CHECK(bytes <= dynamic_smem_bytes() &&
+                   bytes <= (static_cast<uint64_t>(args.nc_mask) + 1u) * (4u * P) && bytes % (4u * P) == 0);
         if ((bytes & 15u) == 0) {
             if (threadIdx.x == 0) mbar_init(&bar, 1);
             __syncthreads();

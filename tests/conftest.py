@@ -6,7 +6,17 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_addoption(parser):
+    parser.addoption("--sage-lib", default=None,
+                     help="load this build of the C-ABI library instead of libsage.so (e.g. the bounds-checked "
+                          "bench/libsage_checked.so)")
+
+
 def pytest_configure(config):
+    lib = config.getoption("--sage-lib")
+    if lib:
+        from paper_2209_03125_b200 import sage
+        sage.load(os.path.abspath(lib))
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libsage.so")
     config.addinivalue_line("markers", "statistical: decided by timing statistics on the GPU (run after the "
                                        "deterministic tests)")

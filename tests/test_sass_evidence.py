@@ -180,3 +180,17 @@ def test_c2a_kernel_op_mix(name, rounds):
     assert d["alu"] <= 30.1, d
     assert d["fma"] <= 26.1 and d["wide"] == 1.0, d
     assert d["hist"].get("LDS", 0) == rounds and d["hist"].get("SHFL.IDX", 0) == rounds, d
+
+
+def test_bounds_checks_compile_out_of_the_product(sass):
+    """The bounds checks (SAGE_CHECK) are in the test-only
+    checked library -- a trap in every checksum kernel -- and nowhere in libsage.so,
+    whose kernels are the same instantiations."""
+    checked = build.build_checked()
+    csass = subprocess.run(["cuobjdump", "-sass", checked], capture_output=True, text=True, check=True).stdout
+    prod, chk = _functions(sass), _functions(csass)
+    assert set(prod) == set(chk)
+    for name, body in prod.items():
+        assert "BPT.TRAP" not in body, name
+        if "sage_checksum_kernel" in name:
+            assert "BPT.TRAP" in chk[name], name
