@@ -13,13 +13,19 @@ def pytest_addoption(parser):
 
 
 def pytest_configure(config):
-    lib = config.getoption("--sage-lib")
-    if lib:
-        from paper_2209_03125_b200 import sage
-        sage.load(os.path.abspath(lib))
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libsage.so")
     config.addinivalue_line("markers", "statistical: decided by timing statistics on the GPU (run after the "
                                        "deterministic tests)")
+    lib = config.getoption("--sage-lib")
+    if lib:
+        from paper_2209_03125_b200 import sage
+        loaded = sage.load(os.path.abspath(lib))
+        assert os.path.realpath(loaded._name) == os.path.realpath(lib), (loaded._name, lib)
+
+
+def pytest_report_header(config):
+    lib = config.getoption("--sage-lib")
+    return ["C-ABI library under test: %s" % os.path.abspath(lib)] if lib else []
 
 
 def pytest_collection_modifyitems(config, items):
