@@ -34,6 +34,14 @@ def test_library_exports_every_declared_symbol(lib):
     assert sorted(sage.EXPORTS) == declared
 
 
+def test_bounds_checked_library_exports_the_same_symbols():
+    """The test-only bounds-checked build (bench/libsage_checked.so, DESIGN.md
+    section 8) is the same C ABI, so the parity suites can run through it."""
+    checked = ctypes.CDLL(build.build_checked())
+    for name in _declared():
+        assert hasattr(checked, name), name
+
+
 def test_strerror_and_codes(lib):
     assert sage.strerror(0) == "ok"
     assert sage.strerror(-1) == "invalid argument"
