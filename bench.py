@@ -477,6 +477,7 @@ def run_ours(args):
                            "placement": placement, "lane_states_per_thread": dbg.ilp,
                            "hw_grid": "%d x %d" % (info.blocks // dbg.ilp, info.threads),
                            "kernel": ctx.kernel_symbol(nbytes, region.data_ptr()),
+                           "kernel_tuned": bool(dbg.tuned),
                            "parallelism": "independent replica per GPU x%d" % ws,
                            "plumbing": backend or "none",
                            "l2": "256 MiB buffer written between timed steps (flush)"},

@@ -99,6 +99,9 @@ typedef struct {
     uint32_t ilp;         /* logical lane states per hardware thread (1 or 2): the launch was
                              blocks/ilp CTAs of `threads`, covering the same blocks*threads
                              logical threads (the c2a kernel uses 2) */
+    uint32_t tuned;       /* 1 if the kernel ran from sage_kernel_tuned.cubin (the c2a kernel with
+                             control-bit-tuned scheduling hints, same instructions, DESIGN.md
+                             section 8); 0 for the kernel embedded in the library */
 } sage_result;
 
 typedef struct {

@@ -16,6 +16,12 @@ LIB = os.path.join(PKG, "libsage.so")
 # the product, kept beside the other test-only library under bench/.
 CHECKED_LIB = os.path.join(ROOT, "bench", "libsage_checked.so")
 CUBIN = os.path.join(PKG, "sage_kernel.cubin")
+# The c2a kernel with control-bit-tuned scheduling hints: the
+# cubin above with the yield hints of csrc/c2a_yield.json applied; the library
+# launches the c2a kernel from it (and falls back to the embedded kernel if it is
+# missing or does not match).
+TUNED_CUBIN = os.path.join(PKG, "sage_kernel_tuned.cubin")
+YIELD_SPEC = os.path.join(CSRC, "c2a_yield.json")
 SOURCES = [os.path.join(CSRC, "sage_api.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "sage_kernel.cuh"), os.path.join(CSRC, "sage_hash.cuh"),
                   os.path.join(INCLUDE, "sage.h")]
@@ -64,7 +70,74 @@ def build(force=False, verbose=False):
         if p.returncode != 0:
             raise RuntimeError("nvcc -cubin failed:\n" + p.stdout + p.stderr)
         os.replace(tmp, CUBIN)
+    build_tuned()
     return LIB
+
+
+def _elf_section(blob, name):
+    """(file offset, size) of ELF64 section `name`, or None."""
+    import struct
+    shoff, = struct.unpack_from("<Q", blob, 0x28)
+    shentsize, shnum, shstrndx = struct.unpack_from("<HHH", blob, 0x3A)
+    hdrs = [struct.unpack_from("<IIQQQQ", blob, shoff + k * shentsize) for k in range(shnum)]
+    stroff = hdrs[shstrndx][4]
+    for nm, _t, _f, _a, off, size in hdrs:
+        end = blob.index(b"\0", stroff + nm)
+        if blob[stroff + nm:end].decode("latin-1") == name:
+            return off, size
+    return None
+
+
+def tuned_cubin(blob, spec):
+    """The cubin `blob` with the spec's yield hints applied (bit `yield_bit` of the
+    high 64-bit word of each listed instruction set to its target value), or None
+    when the kernel's text is not the one the hints were searched on (checked by
+    the SHA-256 of the untuned text): scheduling hints never change what an
+    instruction computes, but they are only known to help that exact schedule."""
+    import hashlib
+    sec = _elf_section(blob, ".text." + spec["function"])
+    if sec is None:
+        return None
+    off, size = sec
+    bit = spec["yield_bit"]
+    text = bytearray(blob[off:off + size])
+    for a, v in spec["yield"].items():               # back to the untuned value for the hash
+        p = int(a) + 8
+        w = int.from_bytes(text[p:p + 8], "little")
+        w = (w | (1 << bit)) if not v else (w & ~(1 << bit))
+        text[p:p + 8] = w.to_bytes(8, "little")
+    if hashlib.sha256(bytes(text)).hexdigest() != spec["untuned_text_sha256"]:
+        return None
+    out = bytearray(blob)
+    for a, v in spec["yield"].items():
+        p = off + int(a) + 8
+        w = int.from_bytes(out[p:p + 8], "little")
+        w = (w | (1 << bit)) if v else (w & ~(1 << bit))
+        out[p:p + 8] = w.to_bytes(8, "little")
+    return bytes(out)
+
+
+def build_tuned():
+    """Write TUNED_CUBIN from CUBIN and YIELD_SPEC (removes it when the spec does not
+    match the build's kernel).  Returns the path or None."""
+    import json
+    if not os.path.exists(YIELD_SPEC) or not os.path.exists(CUBIN):
+        return None
+    spec = json.load(open(YIELD_SPEC))
+    blob = open(CUBIN, "rb").read()
+    out = tuned_cubin(blob, spec)
+    if out is None:
+        if os.path.exists(TUNED_CUBIN):
+            os.remove(TUNED_CUBIN)
+        sys.stderr.write("build: %s does not match the built c2a kernel; the library runs the untuned kernel\n"
+                         % YIELD_SPEC)
+        return None
+    if not os.path.exists(TUNED_CUBIN) or open(TUNED_CUBIN, "rb").read() != out:
+        tmp = TUNED_CUBIN + ".%d.tmp" % os.getpid()
+        with open(tmp, "wb") as f:
+            f.write(out)
+        os.replace(tmp, TUNED_CUBIN)
+    return TUNED_CUBIN
 
 
 def build_checked(force=False):

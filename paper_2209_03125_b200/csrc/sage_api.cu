@@ -4,6 +4,7 @@
 // checksum kernel (sage_kernel.cuh), pinned result readback and host timing
 // (the verifier's t0/t1).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <time.h>
 
 #include <cstdio>
@@ -11,6 +12,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <string>
 #include <utility>
 #include <new>
 
@@ -163,6 +165,7 @@ struct sage_ctx {
     void* d_stage = nullptr;        // device copy of a host region (sage_attest_host)
     size_t stage_bytes = 0;
     uint64_t launches = 0;
+    bool use_tuned = true;          // launch the control-bit-tuned c2a kernel when available
     std::mutex mu;                  // serialises calls that use the ctx-owned buffers
 };
 
@@ -273,16 +276,63 @@ uint32_t choose_placement(const sage_ctx* c, size_t bytes) {
 // device: setting it on every attestation costs host time between back-to-back
 // launches.  Process-wide, guarded by a mutex (contexts may share kernels).
 // force = true re-applies the attribute (after a device reset the cache is stale).
-int ensure_dyn_smem(int device, KernelFn fn, int bytes, bool force = false) {
+int ensure_dyn_smem(int device, const void* fn, int bytes, bool force = false) {
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, int> set;
     std::lock_guard<std::mutex> lock(mu);
-    int& cur = set[{device, reinterpret_cast<const void*>(fn)}];
+    int& cur = set[{device, fn}];
     if (bytes <= cur && !force) return SAGE_OK;
-    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  bytes));
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     cur = bytes;
     return SAGE_OK;
+}
+int ensure_dyn_smem(int device, KernelFn fn, int bytes, bool force = false) {
+    return ensure_dyn_smem(device, reinterpret_cast<const void*>(fn), bytes, force);
+}
+
+// The c2a kernel with control-bit-tuned scheduling hints:
+// sage_kernel_tuned.cubin next to this library holds the same instructions as the
+// embedded c2a kernel with the yield hints of csrc/c2a_yield.json applied (written
+// by the build only when the kernel's text is the one the hints were searched
+// on).  Loaded once per process; used only if it has the embedded kernel's
+// name, registers and static shared memory.  Without the file the embedded
+// (untuned) kernel runs.
+KernelFn c2a_kernel() {
+    return sage::sage_checksum_kernel<1, true, false, XsSmem<1>::xs, kIlpUnroll, Addr<1>::mode, false, kIlpSmem,
+                                      kIlpPad>;
+}
+
+const void* tuned_c2a() {
+    static std::mutex mu;
+    static bool tried = false;
+    static const void* kernel = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (tried) return kernel;
+    tried = true;
+    Dl_info di{};
+    if (!dladdr(reinterpret_cast<void*>(&c2a_kernel), &di) || di.dli_fname == nullptr) return nullptr;
+    std::string path(di.dli_fname);
+    const size_t slash = path.rfind('/');
+    path = (slash == std::string::npos ? std::string(".") : path.substr(0, slash)) + "/sage_kernel_tuned.cubin";
+    FILE* f = fopen(path.c_str(), "rb");
+    if (f == nullptr) return nullptr;
+    fclose(f);
+    const void* untuned = reinterpret_cast<const void*>(c2a_kernel());
+    const char* name = nullptr;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t k = nullptr;
+    cudaFuncAttributes a{}, b{};
+    if (cudaFuncGetName(&name, untuned) != cudaSuccess ||
+        cudaLibraryLoadFromFile(&lib, path.c_str(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&k, lib, name) != cudaSuccess ||
+        cudaFuncGetAttributes(&a, untuned) != cudaSuccess ||
+        cudaFuncGetAttributes(&b, reinterpret_cast<const void*>(k)) != cudaSuccess ||
+        a.numRegs != b.numRegs || a.sharedSizeBytes != b.sharedSizeBytes) {
+        cudaGetLastError();                           // not sticky; the embedded kernel runs
+        return nullptr;
+    }
+    kernel = reinterpret_cast<const void*>(k);
+    return kernel;
 }
 
 // The kernel one attestation of (region, bytes) runs: placement, lane states per
@@ -290,6 +340,7 @@ int ensure_dyn_smem(int device, KernelFn fn, int bytes, bool force = false) {
 // for its address (the 4 GiB straddle test), never dereferenced.
 struct Plan {
     KernelFn fn = nullptr;
+    const void* launch_fn = nullptr;   // what is launched: fn, or its control-bit-tuned copy (c2a)
     uint32_t placement = SAGE_GLOBAL;
     uint32_t ilp = 1;
     size_t dyn = 0;
@@ -325,6 +376,11 @@ int plan_launch(const sage_ctx* c, const void* region, size_t bytes, bool counti
     }
     if (fn == nullptr) return fail(SAGE_EINVAL, "pick_words must be 1, 4 or 8%s");
     out->fn = fn;
+    out->launch_fn = reinterpret_cast<const void*>(fn);
+    if (fn == c2a_kernel() && c->use_tuned) {
+        const void* t = tuned_c2a();
+        if (t) out->launch_fn = t;
+    }
     out->placement = placement;
     out->ilp = ilp;
     out->dyn = smem ? bytes : hybrid ? (bytes < kHybridStage ? bytes : kHybridStage) : 0;
@@ -332,11 +388,12 @@ int plan_launch(const sage_ctx* c, const void* region, size_t bytes, bool counti
 }
 
 int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64_t rounds, uint64_t* raw,
-           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr) {
+           uint64_t* per_warp, uint32_t* placement_used, uint32_t* counts = nullptr, uint32_t* ilp_used = nullptr,
+           uint32_t* tuned_used = nullptr) {
     Plan plan;
     int prc = plan_launch(c, region, bytes, counts != nullptr, &plan);
     if (prc) return prc;
-    const KernelFn fn = plan.fn;
+    const void* fn = plan.launch_fn;
     const uint32_t placement = plan.placement, ilp = plan.ilp;
     const size_t dyn = plan.dyn;
     if (dyn) {
@@ -358,26 +415,31 @@ int launch(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes, uint64
     // one chunk less is staged than its picks can reach, which must trap
     if (dyn && getenv("SAGE_CHECK_SELFTEST")) args.region_bytes -= 4u * c->pick_words;
 #endif
-    fn<<<c->blocks / ilp, c->threads, dyn, c->stream>>>(args);
-    cudaError_t le = cudaGetLastError();
+    void* params[] = {&args};
+    cudaError_t le = cudaLaunchKernel(fn, dim3(c->blocks / ilp), dim3(c->threads), params, dyn, c->stream);
     if (le == cudaErrorInvalidValue && dyn) {
         // the cached shared-memory limit is stale (e.g. cudaDeviceReset): re-apply it once
+        cudaGetLastError();
         int rc = ensure_dyn_smem(c->device, fn, static_cast<int>(dyn), true);
         if (rc) return rc;
-        fn<<<c->blocks / ilp, c->threads, dyn, c->stream>>>(args);
-        le = cudaGetLastError();
+        le = cudaLaunchKernel(fn, dim3(c->blocks / ilp), dim3(c->threads), params, dyn, c->stream);
     }
-    if (le != cudaSuccess) return cuda_fail(le, "checksum kernel launch");
+    if (le != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(le, "checksum kernel launch");
+    }
     c->launches++;
     if (placement_used) *placement_used = placement;
     if (ilp_used) *ilp_used = ilp;
+    if (tuned_used) *tuned_used = fn != reinterpret_cast<const void*>(plan.fn);
     return SAGE_OK;
 }
 
 void fill_result(const sage_ctx* c, const uint64_t raw[4], uint64_t t0, uint64_t t1, uint64_t va, uint32_t placement,
-                 uint32_t ilp, sage_result* out) {
+                 uint32_t ilp, uint32_t tuned, sage_result* out) {
     sage_decode_raw(raw, out);
     out->ilp = ilp;
+    out->tuned = tuned;
     out->elapsed_ns = t1 - t0;
     out->region_va = va;
     out->placement = placement;
@@ -392,13 +454,13 @@ int attest_device(sage_ctx* c, uint64_t nonce, const void* region, size_t bytes,
     const uint64_t t0 = now_ns();
     if (host_src) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(region), host_src, bytes, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_raw, 0, 4 * sizeof(uint64_t), c->stream));
-    uint32_t placement = 0, ilp = 1;
-    int rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts, &ilp);
+    uint32_t placement = 0, ilp = 1, tuned = 0;
+    int rc = launch(c, nonce, region, bytes, rounds, c->d_raw, per_warp, &placement, counts, &ilp, &tuned);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->h_raw, c->d_raw, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     const uint64_t t1 = now_ns();
-    fill_result(c, c->h_raw, t0, t1, reinterpret_cast<uint64_t>(region), placement, ilp, out);
+    fill_result(c, c->h_raw, t0, t1, reinterpret_cast<uint64_t>(region), placement, ilp, tuned, out);
     return SAGE_OK;
 }
 
@@ -423,6 +485,10 @@ int prepare_kernels(const sage_ctx* c) {
     if (rc == SAGE_OK) rc = ensure_dyn_smem(c->device, kernel_for(c->pick_words, true, true), static_cast<int>(kSmemRegionMax));
     if (rc == SAGE_OK && hybrid_geometry(c))
         rc = ensure_dyn_smem(c->device, hybrid_kernel(c->pick_words), static_cast<int>(kHybridStage));
+    if (rc == SAGE_OK && c->use_tuned && kernel_for(c->pick_words, true, false, ilp) == c2a_kernel()) {
+        const void* t = tuned_c2a();
+        if (t) rc = ensure_dyn_smem(c->device, t, static_cast<int>(smem_region_max(c)));
+    }
     return rc;
 }
 
@@ -456,6 +522,7 @@ int sage_checksum_init(const sage_config* cfg, sage_ctx** out) {
     c->blocks = d.blocks ? d.blocks : 2u * static_cast<uint32_t>(sms);
     c->pick_words = d.pick_words;
     c->placement = d.placement;
+    c->use_tuned = getenv("SAGE_NO_TUNED") == nullptr;      // A/B switch
     cudaError_t e;
     if (d.stream) {
         c->stream = static_cast<cudaStream_t>(d.stream);

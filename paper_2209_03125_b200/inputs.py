@@ -44,6 +44,17 @@ def kernel_text(symbol):
     path = os.path.join(_PKG, "sage_kernel.cubin")
     if not os.path.exists(path):
         return b""
+    tuned = os.path.join(_PKG, "sage_kernel_tuned.cubin")
+    if os.path.exists(tuned) and not os.environ.get("SAGE_NO_TUNED"):
+        # the c2a kernel runs from the control-bit-tuned cubin (same instructions,
+        # tuned scheduling hints): its text is the running code
+        with open(tuned, "rb") as f:
+            secs = _elf_sections(f.read())
+        if ".text." + symbol in secs:
+            with open(path, "rb") as f:
+                base = _elf_sections(f.read()).get(".text." + symbol, b"")
+            if secs[".text." + symbol] != base:
+                return bytes(secs[".text." + symbol])
     with open(path, "rb") as f:
         secs = _elf_sections(f.read())
     return bytes(secs.get(".text." + symbol, b""))

@@ -41,7 +41,7 @@ class sage_result(ctypes.Structure):
     _fields_ = [("checksum", ctypes.c_uint64), ("cycles", ctypes.c_uint64), ("elapsed_ns", ctypes.c_uint64),
                 ("device_ns", ctypes.c_uint64), ("region_va", ctypes.c_uint64), ("placement", ctypes.c_uint32),
                 ("blocks", ctypes.c_uint32), ("threads", ctypes.c_uint32), ("pick_words", ctypes.c_uint32),
-                ("ilp", ctypes.c_uint32)]
+                ("ilp", ctypes.c_uint32), ("tuned", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

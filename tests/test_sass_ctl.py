@@ -58,3 +58,30 @@ def test_patch_touches_only_control_bits(probe, tmp_path, mode):
     path = tmp_path / "patched.cubin"
     path.write_bytes(new)
     assert _sass_text(str(path)) == _sass_text(probe.CUBIN)
+
+
+def test_tuned_cubin_differs_only_in_the_specs_yield_hints(probe):
+    """The build's sage_kernel_tuned.cubin (the c2a kernel the library launches,
+    DESIGN.md section 8) is sage_kernel.cubin with bit 45 changed at exactly the
+    instructions csrc/c2a_yield.json lists, all inside the c2a round loop, and the
+    same disassembly."""
+    import json
+    from paper_2209_03125_b200 import build
+    if build.build_tuned() is None:
+        pytest.skip("no yield spec for this build's kernel")
+    spec = json.load(open(build.YIELD_SPEC))
+    base, tuned = open(build.CUBIN, "rb").read(), open(build.TUNED_CUBIN, "rb").read()
+    assert len(base) == len(tuned)
+    off, _ = probe.text_section(base, ".text." + probe.FN)
+    lo, hi = probe.main_loop(build.CUBIN)
+    changed = [i for i in range(len(base)) if base[i] != tuned[i]]
+    want = set()
+    for a, v in spec["yield"].items():
+        a = int(a)
+        assert lo <= a < hi and a % 16 == 0
+        p = off + a + 8
+        wb, wt = (int.from_bytes(x[p:p + 8], "little") for x in (base, tuned))
+        assert wb ^ wt == 1 << 45 and (wt >> 45) & 1 == v
+        want.add(p + 5)                                    # bit 45 lives in byte 5 of the high word
+    assert set(changed) == want
+    assert _sass_text(build.TUNED_CUBIN) == _sass_text(build.CUBIN)
