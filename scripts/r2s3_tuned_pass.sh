@@ -1,4 +1,4 @@
-O=gpurun_out/r2s3_tuned
+O=${O:-gpurun_out/r2s3_tuned}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1
 timeout 600 python -m pytest tests/test_gpu_tuned.py -q -rs > $O/tuned_tests.log 2>&1; echo rc=$? >> $O/tuned_tests.log
