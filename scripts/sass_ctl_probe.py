@@ -35,6 +35,35 @@ CUBIN = os.path.join(ROOT, "paper_2209_03125_b200", "sage_kernel.cubin")
 STALL, YIELD = 41, 45
 
 
+# --target attacker: the adversary test's fastest attacker kernel (+1 IMAD per round,
+# its own searched schedule UNROLL 9 / PAD 1; bench/adversary_lib.cu), compiled to a
+# cubin from the lab template -- to measure how much of the product's hint gain an
+# attacker recovers by running the same search on its own kernel.
+FN_ATTACKER = ("_ZN8sage_lab20sage_checksum_kernelILi1ELb1ELb0ELi16ELi9ELi4ELi0ELin1ELb0ELi1ELi2ELi0ELi1ELi0ELi0ELi0"
+               "ELi0EEEvNS_10KernelArgsE")
+CUBIN_ATTACKER = os.path.join(ROOT, "bench", "adversary_lib.cubin")
+
+
+def build_attacker_cubin():
+    src = os.path.join(ROOT, "bench", "adversary_lib.cu")
+    if not os.path.exists(CUBIN_ATTACKER) or os.path.getmtime(CUBIN_ATTACKER) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(ROOT, "bench", "sage_lab.cuh"))):
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+                               "-std=c++17", "-I" + os.path.join(ROOT, "bench"), "-cubin", "-o", CUBIN_ATTACKER, src])
+    return CUBIN_ATTACKER
+
+
+class LabArgs(ctypes.Structure):             # bench/sage_lab.cuh KernelArgs, natural alignment
+    _fields_ = [("region", ctypes.c_uint64), ("nonce", ctypes.c_uint64), ("nc_mask", ctypes.c_uint32),
+                ("rounds", ctypes.c_uint32), ("region_bytes", ctypes.c_uint32), ("raw", ctypes.c_uint64),
+                ("per_warp", ctypes.c_uint64), ("mul", ctypes.c_uint32 * 16), ("p2", ctypes.c_uint32 * 3),
+                ("four_p", ctypes.c_uint32), ("zero", ctypes.c_uint32), ("one", ctypes.c_uint32),
+                ("counts", ctypes.c_uint64), ("cta_trace", ctypes.c_uint64), ("slice_shift", ctypes.c_uint32),
+                ("progress", ctypes.c_uint64), ("progress_every", ctypes.c_uint32),
+                ("progress_slots", ctypes.c_uint32), ("persist_bytes", ctypes.c_uint64),
+                ("copy_delta", ctypes.c_int64)]
+
+
 class KernelArgs(ctypes.Structure):          # csrc/sage_kernel.cuh KernelArgs, natural alignment
     _fields_ = [("region", ctypes.c_uint64), ("nonce", ctypes.c_uint64), ("nc_mask", ctypes.c_uint32),
                 ("rounds", ctypes.c_uint32), ("region_bytes", ctypes.c_uint32), ("raw", ctypes.c_uint64),
@@ -138,8 +167,12 @@ def main():
     ap.add_argument("--rand", type=int, default=0, help="add this many rand:SEED:P variants")
     ap.add_argument("--p", type=float, default=0.05)
     ap.add_argument("--flipsets", default=None, help="JSON {name: [loop addresses]}: adds set:NAME variants")
+    ap.add_argument("--target", choices=("product", "attacker"), default="product")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    global FN, CUBIN
+    if a.target == "attacker":
+        FN, CUBIN = FN_ATTACKER, build_attacker_cubin()
 
     import torch
     from cuda.bindings import driver as cu
@@ -153,7 +186,7 @@ def main():
     with sage.Context() as ctx:
         info = ctx.query()
         want = ctx.attest(nonce, region, a.rounds).checksum
-        assert ctx.kernel_symbol(8192, region.data_ptr()) == FN
+        assert a.target == "attacker" or ctx.kernel_symbol(8192, region.data_ptr()) == FN
     sms = info.sm_count
     blob = open(CUBIN, "rb").read()
     stream = torch.cuda.current_stream(dev)
@@ -169,8 +202,11 @@ def main():
         err, f = cu.cuModuleGetFunction(mod, FN.encode())
         assert err == cu.CUresult.CUDA_SUCCESS, (mode, err)
         funcs[mode] = (mod, f)
-    args = KernelArgs(region=region.data_ptr(), nonce=nonce, nc_mask=8192 // 4 - 1, rounds=a.rounds,
-                      region_bytes=8192, raw=raw.data_ptr(), per_warp=0, four_p=4, zero=0, one=1, counts=0)
+    Args = LabArgs if a.target == "attacker" else KernelArgs
+    args = Args(region=region.data_ptr(), nonce=nonce, nc_mask=8192 // 4 - 1, rounds=a.rounds,
+                region_bytes=8192, raw=raw.data_ptr(), per_warp=0, four_p=4, zero=0, one=1, counts=0)
+    if a.target == "attacker":
+        args.p2[0], args.p2[1], args.p2[2] = 1 << 20, 1 << 25, 1 << 5
     for j in range(16):
         args.mul[j] = (1 << [5, 11, 3, 17, 9, 23, 7, 13, 29, 2, 19, 6, 15, 27, 4, 21][j]) + 1
     argp = (ctypes.c_void_p * 1)(ctypes.addressof(args))

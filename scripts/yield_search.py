@@ -32,7 +32,10 @@ def main():
     ap.add_argument("--emit-spec", default=None, help="write the best set as the build's yield spec "
                                                      "(paper_2209_03125_b200/csrc/c2a_yield.json)")
     ap.add_argument("--note", default="")
+    ap.add_argument("--target", choices=("product", "attacker"), default="product")
     a = ap.parse_args()
+    if a.target == "attacker":
+        probe.FN, probe.CUBIN = probe.FN_ATTACKER, probe.build_attacker_cubin()
     state = json.load(open(a.state)) if os.path.exists(a.state) else {"best": [], "history": []}
     if a.init is not None and not state["best"]:
         state["best"] = sorted(int(x) for x in a.init.split(",") if x)
