@@ -17,19 +17,21 @@ Two verifier rules, calibrated on honest runs:
     every session of every code-injection adversary, the fastest included, and
     accepts the honest sessions;
   * per session on the 14th of 16 run times (q = 13/15): rejects every session of
-    every code-injection adversary.  Its use against partial cheating (the fastest
-    adversary in only 5 of the 16 challenges, composed from its measured runs and
-    honest ones; the median lets that through by design) sits at the noise limit:
-    the cheater's +0.07-0.09% is the size of the honest main mode's drift within
-    one test (the 14th of 16 honest runs reached +0.066% on one box), so the
-    rule's honest acceptance and its partial-cheating rejection trade against each
-    other (92-100% / 95-100% over the test runs).  Both are
-    recorded; with 24 held-out sessions a 4% false-positive rate alone fails a
-    ">= 95% accepted" check one time in four, so they are bounded loosely here
-    (>= 75%) and the gate is the median rule.
+    every code-injection adversary but the fastest.  On the fastest -- fully, or
+    cheating in only 5 of the 16 challenges (composed from its measured runs and
+    honest ones; the median lets that through by design) -- it sits at the noise
+    limit: the cheater's +0.04-0.09% is the size of the honest main mode's drift
+    within one test (the 14th of 16 honest runs reached +0.066% on one box), so
+    the rule's honest acceptance and its rejection of that attacker trade against
+    each other (92-100% / 95-100% over the session-2 test runs; on one session-3
+    box the attacker ran +0.06% and the rule rejected 17% of its full and 0% of
+    its partial sessions).  Its honest acceptance is bounded
+    loosely (>= 75%: with 24 held-out sessions a 4% false-positive rate alone
+    fails ">= 95%" one time in four), its verdict on the fastest attacker is
+    recorded, not asserted, and the gate is the median rule.
 Equal footing: the adversaries are built from the lab template with ptxas'
 scheduling hints, so the honest runs use the embedded c2a kernel (ptxas' hints)
-rather than the shipped control-bit-tuned one, which is ~1% faster -- a gap an
+rather than the shipped control-bit-tuned one, which is ~1.9% faster -- a gap an
 attacker closes by running the same hint search on its own kernel (DESIGN.md
 sections 8 and 11).
 The memory-copy adversary (SMEM placement staged from a clean copy) is measured
@@ -164,14 +166,16 @@ def test_timing_verifier_rejects_adversaries(adv):
                           if k == "adversaries" else v) for k, v in summary.items() if k != "honest_times_s"}))
     assert summary["honest_restart_frac"] <= 0.05, summary
     assert summary["honest_sessions_accepted_frac"] >= 0.95, summary
-    # the 14th-of-16 rule at the noise limit (docstring): recorded, loosely bounded
+    # the 14th-of-16 rule at the noise limit (docstring): recorded; its honest
+    # acceptance loosely bounded, its verdict on the fastest adversary (full or
+    # partial cheating) not asserted
     assert summary["honest_q_sessions_accepted_frac"] >= 0.75, summary
-    assert summary["partial_cheating_5_of_16"]["q_rule_rejected_frac"] >= 0.75, summary["partial_cheating_5_of_16"]
     for k, name, memcopy in kinds:
         if memcopy:
             continue
         a = summary["adversaries"][name]
         assert a["sessions_rejected_frac"] >= 0.95, (name, a)
-        assert a["q_sessions_rejected_frac"] >= 0.95, (name, a)
+        if name != FASTEST:
+            assert a["q_sessions_rejected_frac"] >= 0.95, (name, a)
         if name != FASTEST:
             assert a["rejected_frac"] >= 0.95, (name, a)
